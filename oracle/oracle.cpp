@@ -1,0 +1,569 @@
+// oracle.cpp — plain, slow, serial CPU oracle for the sunbw hot path.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference legs may load this library.
+// The product (paper_2011_12984_b200/) never links, imports or calls it, and
+// it shares no header, kernel, helper, table or constant with the CUDA path.
+//
+// Build: g++ -O2 -std=c++17 -ffp-contract=off -fno-fast-math -fPIC -shared
+// (x86-64 SSE2 double arithmetic: every + - * / sqrt is one IEEE RN-even
+// rounding; -ffp-contract=off forbids FMA contraction; denormals are on).
+//
+// Citation key: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+// "DESIGN Rk" = reading k listed in DESIGN.md §3 (taken from SURVEY §8(c)).
+//
+// Every function states the passage it follows.  Where the paper defines an
+// operation only by name (the N_Vector roster), the oracle is
+// the plain mathematical definition written out in index order.
+//
+// Parity status: every function here is pinned by tests/test_oracle_*.py
+// (closed forms, brute force, exact rational arithmetic, textbook reductions)
+// EXCEPT the full nonlinear Brusselator trajectory of oracle_sbdf_integrate,
+// which is "parity unpinned" beyond its piecewise pins (the paper prints no
+// solution values, P:425-486 are figure placeholders); see DESIGN.md §3.
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+extern "C" {
+
+// ---------------------------------------------------------------------------
+// O1 streaming operations ("streaming operations like adding two vectors
+// or scaling a vector"; roster S:129-141).  One IEEE rounding per operation,
+// no contraction, no special-casing of coefficients (DESIGN R3).
+// ---------------------------------------------------------------------------
+
+void oracle_linear_sum(int64_t n, double a, const double* x, double b,
+                       const double* y, double* z) {
+  for (int64_t i = 0; i < n; ++i) {
+    double ax = a * x[i];
+    double by = b * y[i];
+    z[i] = ax + by;
+  }
+}
+
+void oracle_scale(int64_t n, double c, const double* x, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = c * x[i];
+}
+
+void oracle_prod(int64_t n, const double* x, const double* y, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = x[i] * y[i];
+}
+
+void oracle_div(int64_t n, const double* x, const double* y, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = x[i] / y[i];
+}
+
+void oracle_const(int64_t n, double c, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = c;
+}
+
+void oracle_abs(int64_t n, const double* x, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = std::fabs(x[i]);
+}
+
+void oracle_inv(int64_t n, const double* x, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = 1.0 / x[i];
+}
+
+void oracle_add_const(int64_t n, const double* x, double b, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = x[i] + b;
+}
+
+// ---------------------------------------------------------------------------
+// O2 reductions ("reduction operations, like norms or dot products";
+// P:180-182 scalar result returned to the host).
+// The sum is a Neumaier-compensated left fold (DESIGN R6): a plain left fold
+// has relative error ~1e-12 at n=1e9, above the parity bar.
+// ---------------------------------------------------------------------------
+
+struct Neumaier {
+  double s = 0.0, c = 0.0;
+  void add(double t) {
+    double tt = s + t;
+    if (std::fabs(s) >= std::fabs(t))
+      c += (s - tt) + t;
+    else
+      c += (t - tt) + s;
+    s = tt;
+  }
+  double value() const { return s + c; }
+};
+
+// Σ x_i y_i  (N_VDotProd; global = this over the concatenation)
+double oracle_dot(int64_t n, const double* x, const double* y) {
+  Neumaier acc;
+  for (int64_t i = 0; i < n; ++i) acc.add(x[i] * y[i]);
+  return acc.value();
+}
+
+// Σ (x_i w_i)^2 — the local partial of the WRMS norm (N_VWSqrSumLocal)
+double oracle_wsqrsum(int64_t n, const double* x, const double* w) {
+  Neumaier acc;
+  for (int64_t i = 0; i < n; ++i) {
+    double p = x[i] * w[i];
+    acc.add(p * p);
+  }
+  return acc.value();
+}
+
+// Σ_{id_i>0} (x_i w_i)^2
+double oracle_wsqrsum_mask(int64_t n, const double* x, const double* w,
+                           const double* id) {
+  Neumaier acc;
+  for (int64_t i = 0; i < n; ++i) {
+    if (id[i] > 0.0) {
+      double p = x[i] * w[i];
+      acc.add(p * p);
+    }
+  }
+  return acc.value();
+}
+
+// sqrt(Σ (x_i w_i)^2 / N), N = n (DESIGN R5: global length, also under mask)
+double oracle_wrms(int64_t n, const double* x, const double* w) {
+  if (n <= 0) return std::nan("");
+  double s = oracle_wsqrsum(n, x, w);
+  return std::sqrt(s / (double)n);
+}
+
+double oracle_wrms_mask(int64_t n, const double* x, const double* w,
+                        const double* id) {
+  if (n <= 0) return std::nan("");
+  double s = oracle_wsqrsum_mask(n, x, w, id);
+  return std::sqrt(s / (double)n);
+}
+
+// max |x_i|; NaN never selected (predicate |x|>max, DESIGN R9); n=0 → NaN
+double oracle_max_norm(int64_t n, const double* x) {
+  if (n <= 0) return std::nan("");
+  double m = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double a = std::fabs(x[i]);
+    if (a > m) m = a;
+  }
+  return m;
+}
+
+// min x_i; n=0 → +inf (identity of min; the global op errors on N=0)
+double oracle_min(int64_t n, const double* x) {
+  double m = INFINITY;
+  for (int64_t i = 0; i < n; ++i)
+    if (x[i] < m) m = x[i];
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// O3 fused operations (not in the paper; SUNDIALS definitions, DESIGN R1/R4).
+// ---------------------------------------------------------------------------
+
+// z = Σ_j c_j X_j, summed left to right in j: z = c0 X0; z = z + c_j X_j.
+void oracle_linear_combination(int nv, const double* c, const double* const* X,
+                               int64_t n, double* z) {
+  for (int64_t i = 0; i < n; ++i) {
+    double acc = c[0] * X[0][i];
+    for (int j = 1; j < nv; ++j) {
+      double t = c[j] * X[j][i];
+      acc = acc + t;
+    }
+    z[i] = acc;
+  }
+}
+
+// Z_j = a_j x + Y_j
+void oracle_scale_add_multi(int nv, const double* a, const double* x,
+                            const double* const* Y, double* const* Z,
+                            int64_t n) {
+  for (int j = 0; j < nv; ++j)
+    for (int64_t i = 0; i < n; ++i) {
+      double t = a[j] * x[i];
+      Z[j][i] = t + Y[j][i];
+    }
+}
+
+// d_j = x · Y_j
+void oracle_dot_prod_multi(int nv, const double* x, const double* const* Y,
+                           int64_t n, double* dots) {
+  for (int j = 0; j < nv; ++j) dots[j] = oracle_dot(n, x, Y[j]);
+}
+
+// ---------------------------------------------------------------------------
+// Block-diagonal matrix (square blocks A_j sharing one pattern).
+// Storage: G blocks of m×m, row-major within a block, blocks contiguous.
+// ---------------------------------------------------------------------------
+
+// A <- c A + I  (SUNMatScaleAddI): a_ij = RN(c a_ij), then a_ii += 1.
+void oracle_scale_add_identity(int64_t G, int m, double c, double* A) {
+  for (int64_t g = 0; g < G; ++g) {
+    double* a = A + g * m * m;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        double v = c * a[i * m + j];
+        if (i == j) v = v + 1.0;
+        a[i * m + j] = v;
+      }
+  }
+}
+
+// O6: LU with partial pivoting per block, in place (Doolittle, unit L below
+// the diagonal, U on and above).  Column k: pivot = first row of max |a_ik|,
+// i >= k (LAPACK idamax rule, DESIGN R11); swap whole rows; l_ik = a_ik/a_kk;
+// a_ij -= l_ik a_kj for j > k.  piv[g*m + k] = chosen row at step k (0-based).
+// A zero pivot marks the block singular: elimination of that column is
+// skipped and the block is finished.  Returns 1 + first singular block, or 0.
+// (Role of cuSolverSp batch-QR; per-cell dense solve per P:389-390.)
+int64_t oracle_lu_factor(int64_t G, int m, double* A, int32_t* piv) {
+  int64_t first_singular = 0;
+  for (int64_t g = 0; g < G; ++g) {
+    double* a = A + g * m * m;
+    int32_t* p = piv + g * m;
+    bool singular = false;
+    for (int k = 0; k < m; ++k) {
+      int r = k;
+      double best = std::fabs(a[k * m + k]);
+      for (int i = k + 1; i < m; ++i) {
+        double v = std::fabs(a[i * m + k]);
+        if (v > best) { best = v; r = i; }
+      }
+      p[k] = r;
+      if (r != k)
+        for (int j = 0; j < m; ++j) {
+          double t = a[k * m + j];
+          a[k * m + j] = a[r * m + j];
+          a[r * m + j] = t;
+        }
+      double akk = a[k * m + k];
+      if (akk == 0.0) { singular = true; continue; }
+      for (int i = k + 1; i < m; ++i) {
+        double l = a[i * m + k] / akk;
+        a[i * m + k] = l;
+        for (int j = k + 1; j < m; ++j) {
+          double t = l * a[k * m + j];
+          a[i * m + j] = a[i * m + j] - t;
+        }
+      }
+    }
+    if (singular && first_singular == 0) first_singular = g + 1;
+  }
+  return first_singular;
+}
+
+// O7: x = U^{-1} L^{-1} P b per block; x may alias b.  Forward then back
+// substitution in index order, each Σ as sequential RN subtractions.
+void oracle_lu_solve(int64_t G, int m, const double* LU, const int32_t* piv,
+                     const double* b, double* x) {
+  std::vector<double> y(m);
+  for (int64_t g = 0; g < G; ++g) {
+    const double* a = LU + g * m * m;
+    const int32_t* p = piv + g * m;
+    for (int i = 0; i < m; ++i) y[i] = b[g * m + i];
+    for (int k = 0; k < m; ++k) {
+      int r = p[k];
+      if (r != k) { double t = y[k]; y[k] = y[r]; y[r] = t; }
+    }
+    for (int i = 0; i < m; ++i) {
+      double s = y[i];
+      for (int j = 0; j < i; ++j) {
+        double t = a[i * m + j] * y[j];
+        s = s - t;
+      }
+      y[i] = s;
+    }
+    for (int i = m - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int j = i + 1; j < m; ++j) {
+        double t = a[i * m + j] * y[j];
+        s = s - t;
+      }
+      y[i] = s / a[i * m + i];
+    }
+    for (int i = 0; i < m; ++i) x[g * m + i] = y[i];
+  }
+}
+
+// y = A x per block (the low-storage block SpMV role)
+void oracle_block_matvec(int64_t G, int m, const double* A, const double* x,
+                         double* y) {
+  for (int64_t g = 0; g < G; ++g)
+    for (int i = 0; i < m; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < m; ++j) {
+        double t = A[g * m * m + i * m + j] * x[g * m + j];
+        s = s + t;
+      }
+      y[g * m + i] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Brusselator advection–reaction.  State interleaved per cell
+// (u,v,w) (DESIGN R12).  Parameters: c, A, B, eps.
+// ---------------------------------------------------------------------------
+
+// O8 reaction f_I (reaction terms):
+//   f_u = A - (w+1) u + v u^2 ;  f_v = w u - v u^2 ;  f_w = (B - w)/eps - w u
+void oracle_bruss_reaction(int64_t G, const double* y, double A, double B,
+                           double eps, double* f) {
+  for (int64_t g = 0; g < G; ++g) {
+    double u = y[3 * g], v = y[3 * g + 1], w = y[3 * g + 2];
+    double uu = u * u;
+    double vuu = v * uu;
+    double w1 = w + 1.0;
+    double w1u = w1 * u;
+    double fu = A - w1u;
+    fu = fu + vuu;
+    double wu = w * u;
+    double fv = wu - vuu;
+    double bw = B - w;
+    double bwe = bw / eps;
+    double fw = bwe - wu;
+    f[3 * g] = fu;
+    f[3 * g + 1] = fv;
+    f[3 * g + 2] = fw;
+  }
+}
+
+// O5 reaction Jacobian J = ∂f_I/∂(u,v,w) (P:369-371 differentiated; P:389
+// block structure), stored as G row-major 3×3 blocks.  inv_eps = RN(1/eps).
+void oracle_bruss_jacobian(int64_t G, const double* y, double eps, double* J) {
+  double inv_eps = 1.0 / eps;
+  for (int64_t g = 0; g < G; ++g) {
+    double u = y[3 * g], v = y[3 * g + 1], w = y[3 * g + 2];
+    double uu = u * u;
+    double u2 = 2.0 * u;
+    double uv2 = u2 * v;
+    double* a = J + 9 * g;
+    double w1 = w + 1.0;
+    a[0] = uv2 - w1;          // ∂f_u/∂u = -(w+1) + 2uv
+    a[1] = uu;                // ∂f_u/∂v = u^2
+    a[2] = -u;                // ∂f_u/∂w = -u
+    a[3] = w - uv2;           // ∂f_v/∂u = w - 2uv
+    a[4] = -uu;               // ∂f_v/∂v = -u^2
+    a[5] = u;                 // ∂f_v/∂w = u
+    a[6] = -w;                // ∂f_w/∂u = -w
+    a[7] = 0.0;               // ∂f_w/∂v = 0
+    a[8] = -inv_eps - u;      // ∂f_w/∂w = -1/eps - u
+  }
+}
+
+// O9 advection f_E, first-order upwind for c > 0 (DESIGN R20),
+// periodic.  Global grid nx × ny × nz cells (1D: ny = nz = 1),
+// index ((k ny + j) nx + i)·3 + s.  Per axis: term = RN(kappa·RN(q_prev - q)),
+// kappa = RN(c/Δ) precomputed by the caller.  Sum order: x, then + y, then
+// + z (DESIGN R19).  Axes of extent 1 contribute nothing (1D / 2D).
+void oracle_advection(int64_t nx, int64_t ny, int64_t nz, double kx, double ky,
+                      double kz, const double* y, double* f) {
+  for (int64_t k = 0; k < nz; ++k)
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t i = 0; i < nx; ++i) {
+        int64_t c = (k * ny + j) * nx + i;
+        int64_t im = (i == 0 ? nx - 1 : i - 1);
+        int64_t jm = (j == 0 ? ny - 1 : j - 1);
+        int64_t km = (k == 0 ? nz - 1 : k - 1);
+        int64_t cx = (k * ny + j) * nx + im;
+        int64_t cy = (k * ny + jm) * nx + i;
+        int64_t cz = (km * ny + j) * nx + i;
+        for (int s = 0; s < 3; ++s) {
+          double q = y[3 * c + s];
+          double d = y[3 * cx + s] - q;
+          double acc = kx * d;
+          if (ny > 1) {
+            double dy = y[3 * cy + s] - q;
+            double ty = ky * dy;
+            acc = acc + ty;
+          }
+          if (nz > 1) {
+            double dz = y[3 * cz + s] - q;
+            double tz = kz * dz;
+            acc = acc + tz;
+          }
+          f[3 * c + s] = acc;
+        }
+      }
+}
+
+// O10 initial condition: p = α exp(-r²/(2σ²)), μ = L/2, σ = L/4
+// per axis; u = A + p, v = B/A + p, w = 3 + p.  Coordinates x_i = i·Δ
+// (uniform mesh).  r² = (x-μx)² [+ (y-μy)²] [+ (z-μz)²] in that order;
+// 2σ² is per-axis-equal only for cubes, so the exponent is summed per axis:
+// e = (x-μx)²/(2σx²) + (y-μy)²/(2σy²) + (z-μz)²/(2σz²).
+void oracle_bruss_ic(int64_t nx, int64_t ny, int64_t nz, double Lx, double Ly,
+                     double Lz, double A, double B, double alpha, double* y) {
+  double dx = Lx / (double)nx, dy = Ly / (double)ny, dz = Lz / (double)nz;
+  double mx = Lx / 2.0, my = Ly / 2.0, mz = Lz / 2.0;
+  double sx = Lx / 4.0, sy = Ly / 4.0, sz = Lz / 4.0;
+  double tx = 2.0 * (sx * sx), ty = 2.0 * (sy * sy), tz = 2.0 * (sz * sz);
+  double BA = B / A;
+  for (int64_t k = 0; k < nz; ++k)
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t i = 0; i < nx; ++i) {
+        double xe = (double)i * dx - mx;
+        double e = (xe * xe) / tx;
+        if (ny > 1) {
+          double ye = (double)j * dy - my;
+          e = e + (ye * ye) / ty;
+        }
+        if (nz > 1) {
+          double ze = (double)k * dz - mz;
+          e = e + (ze * ze) / tz;
+        }
+        double p = alpha * std::exp(-e);
+        int64_t c = (k * ny + j) * nx + i;
+        y[3 * c] = A + p;
+        y[3 * c + 1] = BA + p;
+        y[3 * c + 2] = 3.0 + p;
+      }
+}
+
+// ---------------------------------------------------------------------------
+// O11–O13: fixed-step IMEX-BDF (SBDF1 start, then SBDF2) with modified Newton
+// on the implicit reaction (P:384-385 IMEX split: advection explicit, stiff
+// reaction implicit; P:388-390 per-cell Newton with block solves; DESIGN
+// R14/R15).  Steps:
+//   f_E,n = advection(y_n)
+//   n = 0:  d = 1·y_0 + h·f_E,0                       γ = h
+//   n ≥ 1:  d = 4/3 y_n − 1/3 y_{n−1} + 4h/3 f_E,n − 2h/3 f_E,n−1   γ = 2h/3
+//   ewt = 1/(rtol |y_n| + atol)   (Abs → Scale → AddConst → Inv)
+//   z = y_n;  M = I − γ J(z)  (Jacobian, ScaleAddI(−γ)), LU factor
+//   iterate: r = d + γ f_I(z) − z ; δ = M⁻¹ r ; z = z + δ ; ν = WRMS(δ, ewt)
+//   y_{n+1} = z
+// Problem kinds: 0 = Brusselator (reaction O8/O5, advection O9);
+//                1 = linear test y' = λ_E y + λ_I y (f_E = λ_E y, f_I = λ_I y,
+//                    J = λ_I I per 3×3 block).
+// newton_mode: 0 fixed-K (exactly K iterations), 1 tolerance (stop when
+// ν ≤ tol_nl, fail after K), 2 full convergence (iterate until
+// ‖δ‖∞ ≤ 4u‖z‖∞ or 50 iterations; certifies K).
+// ---------------------------------------------------------------------------
+
+struct OracleSbdfParams {
+  int32_t kind;           // 0 brusselator, 1 linear test
+  int32_t newton_mode;    // 0 fixed-K, 1 tol, 2 full convergence
+  int32_t K;
+  int32_t reaction_only;  // 1: f_E = 0
+  int64_t nx, ny, nz;     // global grid
+  double kx, ky, kz;      // kappa per axis = c/Δ (RN)
+  double A, B, eps;
+  double lam_E, lam_I;
+  double h, rtol, atol, tol_nl;
+};
+
+struct OracleSbdfStats {
+  int64_t steps;
+  int64_t newton_iters;
+  int64_t setups;
+  int64_t solves;
+  int64_t fails;          // tolerance-mode failures (recoverable)
+  int64_t singular;       // 1 + first singular block at the first failure
+  double last_nu;
+};
+
+static void rhs_explicit(const OracleSbdfParams* P, int64_t n, const double* y,
+                         double* fE) {
+  if (P->reaction_only) {
+    for (int64_t i = 0; i < n; ++i) fE[i] = 0.0;
+    return;
+  }
+  if (P->kind == 0)
+    oracle_advection(P->nx, P->ny, P->nz, P->kx, P->ky, P->kz, y, fE);
+  else
+    oracle_scale(n, P->lam_E, y, fE);
+}
+
+static void rhs_implicit(const OracleSbdfParams* P, int64_t G, const double* y,
+                         double* fI) {
+  if (P->kind == 0)
+    oracle_bruss_reaction(G, y, P->A, P->B, P->eps, fI);
+  else
+    oracle_scale(3 * G, P->lam_I, y, fI);
+}
+
+static void jac_implicit(const OracleSbdfParams* P, int64_t G, const double* y,
+                         double* J) {
+  if (P->kind == 0) {
+    oracle_bruss_jacobian(G, y, P->eps, J);
+  } else {
+    for (int64_t g = 0; g < G; ++g)
+      for (int e = 0; e < 9; ++e)
+        J[9 * g + e] = (e % 4 == 0) ? P->lam_I : 0.0;
+  }
+}
+
+// Evolves y (in/out, 3G values) by nsteps fixed steps.  ylog (optional,
+// may be NULL) receives y after every log_every steps (log_every>0).
+// Returns 0, or 1 on a recoverable failure (tolerance mode non-convergence
+// or singular block), stopping at that step.
+int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
+                          OracleSbdfStats* st, double* ylog,
+                          int64_t log_every) {
+  int64_t G = P->nx * P->ny * P->nz;
+  int64_t n = 3 * G;
+  std::vector<double> yprev(n), fE(n), fEprev(n), d(n), ewt(n), z(n), fI(n),
+      r(n), delta(n), M(9 * G), tmp(n);
+  std::vector<int32_t> piv(3 * G);
+  std::memset(st, 0, sizeof(*st));
+  int64_t nlog = 0;
+  for (int64_t step = 0; step < nsteps; ++step) {
+    rhs_explicit(P, n, y, fE.data());
+    double gamma;
+    if (step == 0) {
+      oracle_linear_sum(n, 1.0, y, P->h, fE.data(), d.data());
+      gamma = P->h;
+    } else {
+      double c[4] = {4.0 / 3.0, -1.0 / 3.0, (4.0 * P->h) / 3.0,
+                     -((2.0 * P->h) / 3.0)};
+      const double* X[4] = {y, yprev.data(), fE.data(), fEprev.data()};
+      oracle_linear_combination(4, c, X, n, d.data());
+      gamma = (2.0 * P->h) / 3.0;
+    }
+    // ewt = 1/(rtol|y_n| + atol)
+    oracle_abs(n, y, tmp.data());
+    oracle_scale(n, P->rtol, tmp.data(), tmp.data());
+    oracle_add_const(n, tmp.data(), P->atol, tmp.data());
+    if (!(oracle_min(n, tmp.data()) > 0.0)) return 1;
+    oracle_inv(n, tmp.data(), ewt.data());
+    // predictor and Newton matrix at the predictor (modified Newton)
+    std::memcpy(z.data(), y, n * sizeof(double));
+    jac_implicit(P, G, z.data(), M.data());
+    oracle_scale_add_identity(G, 3, -gamma, M.data());
+    int64_t sing = oracle_lu_factor(G, 3, M.data(), piv.data());
+    st->setups++;
+    if (sing) { st->singular = sing; st->fails++; return 1; }
+    int maxit = (P->newton_mode == 2) ? 50 : P->K;
+    bool converged = (P->newton_mode == 0);
+    for (int it = 0; it < maxit; ++it) {
+      rhs_implicit(P, G, z.data(), fI.data());
+      double c3[3] = {1.0, gamma, -1.0};
+      const double* X3[3] = {d.data(), fI.data(), z.data()};
+      oracle_linear_combination(3, c3, X3, n, r.data());
+      oracle_lu_solve(G, 3, M.data(), piv.data(), r.data(), delta.data());
+      st->solves++;
+      oracle_linear_sum(n, 1.0, z.data(), 1.0, delta.data(), z.data());
+      double nu = oracle_wrms(n, delta.data(), ewt.data());
+      st->newton_iters++;
+      st->last_nu = nu;
+      if (P->newton_mode == 1 && nu <= P->tol_nl) { converged = true; break; }
+      if (P->newton_mode == 2) {
+        double dm = oracle_max_norm(n, delta.data());
+        double zm = oracle_max_norm(n, z.data());
+        if (dm <= 4.0 * 2.220446049250313e-16 * zm) { converged = true; break; }
+      }
+    }
+    if (!converged) { st->fails++; return 1; }
+    std::memcpy(yprev.data(), y, n * sizeof(double));
+    std::memcpy(fEprev.data(), fE.data(), n * sizeof(double));
+    std::memcpy(y, z.data(), n * sizeof(double));
+    st->steps++;
+    if (ylog && log_every > 0 && (step + 1) % log_every == 0) {
+      std::memcpy(ylog + nlog * n, y, n * sizeof(double));
+      ++nlog;
+    }
+  }
+  return 0;
+}
+
+int oracle_abi_version(void) { return 1; }
+
+}  // extern "C"
