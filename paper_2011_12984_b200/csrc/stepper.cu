@@ -1,0 +1,426 @@
+// stepper.cu — fixed-step IMEX-BDF Newton driver (the integrator + task-local
+// nonlinear solver of the paper's demonstration, §7).
+//
+// IMEX split: advection f_E explicit, stiff reaction f_I
+// implicit.  Integrator (DESIGN R14): SBDF1 on the first step, SBDF2 after:
+//   n = 0:  z - h f_I(z) = y_0 + h f_E(y_0)                       (γ = h)
+//   n ≥ 1:  z - (2h/3) f_I(z) = 4/3 y_n - 1/3 y_{n-1}
+//                               + 4h/3 f_E(y_n) - 2h/3 f_E(y_{n-1})  (γ = 2h/3)
+// Nonlinear solver (DESIGN R15): modified Newton per cell,
+// matrix M = I - γ J(z⁰) built and LU-factored once per step at the
+// predictor z⁰ = y_n; each iteration r = d + γ f_I(z) - z, δ = M⁻¹ r,
+// z += δ, ν = WRMS(δ, ewt), ewt = 1/(rtol |y_n| + atol).
+//
+// Composed mode: every stage is one of the library's N_Vector / matrix /
+// solver kernels, enqueued on the context stream (the structure of
+// fig:advrecatorg).  Fixed-K mode never synchronises inside a
+// step; the step is captured once per buffer-rotation state into a CUDA
+// graph and replayed (launch-bound small problems).  Tolerance
+// mode synchronises once per Newton iteration for the host decision
+// (reductions return to the host).
+//
+// Fused mode (the task-local solver as ONE kernel per step):
+// after the halo + advection kernels, each thread owns one cell and runs the
+// whole step — d, ewt, Jacobian, M, LU, K Newton iterations — in registers,
+// with the same operation order as the composed path (bit-identical state);
+// per-iteration WRMS and the ewt minimum leave as per-CTA partials folded by
+// one small kernel.
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "sunbw_internal.h"
+
+namespace sunbw {
+int bw_reaction(void* prob, const double* y, double* f);
+int bw_jacobian(void* prob, const double* y, double* J);
+int bw_halo(void* prob, const double* y);
+int bw_advection_stencil(void* prob, const double* y, double* f);
+int64_t bw_local_cells(void* prob);
+int lu_factor_noreset(SUNBW_Context, int64_t G, int m, double* A, int32_t* piv,
+                      unsigned long long* d_first);
+int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, double h,
+                 double rtol, double atol, const double* y, const double* yp, const double* fE,
+                 const double* fEp, double* z, double* partials, unsigned long long* d_first,
+                 int* nblocks_out);
+int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
+               double* d_min, double* d_nu, int* d_err);
+}  // namespace sunbw
+
+namespace {
+
+constexpr int kMaxK = 32;
+
+struct Stepper {
+  void* prob;
+  SUNBW_Context ctx;
+  BW_StepperOptions opt;
+  int64_t G, n, nglobal;
+  double* y[3];
+  double* fE[2];
+  int iy = 0, iyp = 1, iz = 2, ife = 0, ifep = 1;
+  double *d, *ewt, *tmp, *fI, *r, *delta, *M;
+  int32_t* piv;
+  unsigned long long* d_first;
+  double* d_scal;        // [0] ewt min, [1..K] nu per iteration
+  int* d_err;            // 1: non-positive ewt denominator seen
+  double* d_partials;    // fused mode per-CTA partials
+  int64_t step = 0;
+  double t = 0.0;
+  BW_StepperStats st{};
+  // graphs, keyed by rotation state (iy, ife): 3 × 2
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec[6] = {};
+  int64_t graph_launches[6] = {};
+  // timing
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_kind;
+  double k_ms[BW_K_COUNT_] = {};
+  int64_t k_count[BW_K_COUNT_] = {};
+};
+
+int alloc(Stepper* S, double** p, int64_t count) {
+  if (cudaMalloc(p, sizeof(double) * (count > 0 ? count : 1)) != cudaSuccess) {
+    cudaGetLastError();
+    return SUNBW_ERR_MEM;
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------ timing hooks
+struct Timed {
+  Stepper* S;
+  int kind;
+  bool on;
+  Timed(Stepper* s, int k) : S(s), kind(k), on(s->opt.timing != 0) {
+    if (!on) return;
+    if (S->ev_used + 2 > S->ev_pool.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        S->ev_pool.push_back(e);
+      }
+    }
+    cudaEventRecord(S->ev_pool[S->ev_used], S->ctx->stream);
+  }
+  ~Timed() {
+    if (!on) return;
+    cudaEventRecord(S->ev_pool[S->ev_used + 1], S->ctx->stream);
+    S->ev_kind.push_back(kind);
+    S->ev_used += 2;
+  }
+};
+
+void harvest_timing(Stepper* S) {
+  for (size_t i = 0; i < S->ev_kind.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, S->ev_pool[2 * i], S->ev_pool[2 * i + 1]);
+    S->k_ms[S->ev_kind[i]] += ms;
+    S->k_count[S->ev_kind[i]]++;
+  }
+  S->ev_kind.clear();
+  S->ev_used = 0;
+}
+
+#define TRY(x)              \
+  do {                      \
+    int e_ = (x);           \
+    if (e_ < 0) return e_;  \
+  } while (0)
+
+// ------------------------------------------------------------- one step
+// Enqueues the whole step on ctx->stream.  Tolerance mode: returns > 0 on a
+// recoverable failure (needs the host decision, so it synchronises).
+int enqueue_step(Stepper* S, bool first) {
+  SUNBW_Context ctx = S->ctx;
+  const BW_StepperOptions& o = S->opt;
+  const int64_t n = S->n, G = S->G;
+  double* y = S->y[S->iy];
+  double* yp = S->y[S->iyp];
+  double* z = S->y[S->iz];
+  double* fE = S->fE[S->ife];
+  double* fEp = S->fE[S->ifep];
+  const double h = o.h;
+  const double gamma = first ? h : (2.0 * h) / 3.0;
+
+  { Timed t(S, BW_K_HALO); TRY(sunbw::bw_halo(S->prob, y)); }
+  { Timed t(S, BW_K_ADVECTION); TRY(sunbw::bw_advection_stencil(S->prob, y, fE)); }
+
+  if (o.fused) {
+    int nb = 0;
+    {
+      Timed t(S, BW_K_FUSED_NEWTON);
+      TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
+                              S->d_partials, S->d_first, &nb));
+    }
+    { Timed t(S, BW_K_WRMS); TRY(sunbw::fused_fold(ctx, S->d_partials, nb, o.K, S->nglobal, S->d_scal,
+                                                  S->d_scal + 1, S->d_err)); }
+    return 0;
+  }
+
+  {
+    Timed t(S, BW_K_RHS_COMBINE);
+    if (first) {
+      TRY(sunbw::linear_sum(ctx, n, 1.0, y, h, fE, S->d, nullptr));
+    } else {
+      const double c[4] = {4.0 / 3.0, -1.0 / 3.0, (4.0 * h) / 3.0, -((2.0 * h) / 3.0)};
+      const double* X[4] = {y, yp, fE, fEp};
+      TRY(sunbw::linear_combination(ctx, n, 4, c, X, S->d, nullptr));
+    }
+  }
+  {
+    Timed t(S, BW_K_EWT);
+    TRY(sunbw::abs_(ctx, n, y, S->tmp, nullptr));
+    TRY(sunbw::scale(ctx, n, o.rtol, S->tmp, S->tmp, nullptr));
+    TRY(sunbw::add_const(ctx, n, S->tmp, o.atol, S->tmp, nullptr));
+    TRY(sunbw::reduce(ctx, sunbw::RK_MIN, sunbw::RF_NONE, n, S->nglobal, S->tmp, nullptr, nullptr,
+                      S->d_scal, nullptr, true, nullptr));
+    TRY(sunbw::flag_nonpositive(ctx, S->d_scal, S->d_err));
+    TRY(sunbw::inv(ctx, n, S->tmp, S->ewt, nullptr));
+  }
+  { Timed t(S, BW_K_PREDICT); TRY(sunbw::scale(ctx, n, 1.0, y, z, nullptr)); }
+  { Timed t(S, BW_K_JACOBIAN); TRY(sunbw::bw_jacobian(S->prob, z, S->M)); }
+  { Timed t(S, BW_K_SCALEADDI); TRY(sunbw::scale_add_identity(ctx, G, 3, -gamma, S->M)); }
+  { Timed t(S, BW_K_LU_SETUP); TRY(sunbw::lu_factor_noreset(ctx, G, 3, S->M, S->piv, S->d_first)); }
+
+  const bool tol = o.newton_mode == 1;
+  if (tol) {
+    // the host needs the singular flag and the ewt check before iterating
+    unsigned long long f = 0;
+    int err = 0;
+    if (cudaMemcpyAsync(&f, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(&err, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    if (err) return SUNBW_RECOV_BAD_EWT;
+    if (f != ~0ull) { S->st.singular = (int64_t)f; return SUNBW_RECOV_SINGULAR; }
+  }
+  const double c3[3] = {1.0, gamma, -1.0};
+  for (int it = 0; it < o.K; ++it) {
+    { Timed t(S, BW_K_REACTION); TRY(sunbw::bw_reaction(S->prob, z, S->fI)); }
+    {
+      Timed t(S, BW_K_RESIDUAL);
+      const double* X3[3] = {S->d, S->fI, z};
+      TRY(sunbw::linear_combination(ctx, n, 3, c3, X3, S->r, nullptr));
+    }
+    { Timed t(S, BW_K_LU_SOLVE); TRY(sunbw::lu_solve(ctx, G, 3, S->M, S->piv, S->r, S->delta)); }
+    { Timed t(S, BW_K_UPDATE); TRY(sunbw::linear_sum(ctx, n, 1.0, z, 1.0, S->delta, z, nullptr)); }
+    {
+      Timed t(S, BW_K_WRMS);
+      TRY(sunbw::reduce(ctx, sunbw::RK_WSQR, sunbw::RF_WRMS, n, S->nglobal, S->delta, S->ewt, nullptr,
+                        S->d_scal + 1 + it, tol ? ctx->h_slot_dev : nullptr, true, nullptr));
+    }
+    S->st.newton_iters++;
+    S->st.solves++;
+    if (tol) {
+      if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      double nu = ((volatile double*)ctx->h_slot)[0];
+      S->st.last_nu = nu;
+      if (nu <= o.tol_nl) return 0;        // all ranks see the same global ν (R17)
+    }
+  }
+  return tol ? SUNBW_RECOV_NONCONV : 0;
+}
+
+void rotate(Stepper* S) {
+  int oy = S->iy, oyp = S->iyp, oz = S->iz;
+  S->iy = oz; S->iyp = oy; S->iz = oyp;
+  std::swap(S->ife, S->ifep);
+}
+
+int graph_key(const Stepper* S) { return S->iy * 2 + S->ife; }
+
+// capture one SBDF2 step (fixed-K) for the current rotation state
+int capture_step(Stepper* S, int key) {
+  SUNBW_Context ctx = S->ctx;
+  if (!S->cap_stream &&
+      cudaStreamCreateWithFlags(&S->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  cudaStream_t user = ctx->stream;
+  ctx->stream = S->cap_stream;
+  int64_t l0 = ctx->launches.load();
+  int64_t it0 = S->st.newton_iters, so0 = S->st.solves;
+  cudaGraph_t g = nullptr;
+  int rc = 0;
+  if (cudaStreamBeginCapture(S->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    rc = SUNBW_ERR_CUDA;
+  } else {
+    rc = enqueue_step(S, false);
+    if (cudaStreamEndCapture(S->cap_stream, &g) != cudaSuccess) rc = rc ? rc : SUNBW_ERR_CUDA;
+  }
+  ctx->stream = user;
+  S->st.newton_iters = it0;
+  S->st.solves = so0;
+  S->graph_launches[key] = ctx->launches.load() - l0;
+  ctx->launches -= S->graph_launches[key];
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return ctx_set_err(ctx, rc < 0 ? rc : SUNBW_ERR_CUDA);
+  }
+  if (cudaGraphInstantiate(&S->gexec[key], g, 0) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  }
+  cudaGraphDestroy(g);
+  return 0;
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions* opt, void** out) {
+  if (!prob || !y0 || !opt || !out) return SUNBW_ERR_ARG;
+  *out = nullptr;
+  if (opt->K < 1 || opt->K > kMaxK || !(opt->h > 0) || (opt->newton_mode != 0 && opt->newton_mode != 1))
+    return SUNBW_ERR_ARG;
+  if (opt->fused && (opt->newton_mode != 0 || opt->K > 8)) return SUNBW_ERR_UNSUPPORTED;
+  SUNBW_Context ctx = y0->ctx;
+  int64_t G = sunbw::bw_local_cells(prob);
+  if (y0->local_len != 3 * G) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
+  auto* S = new Stepper();
+  S->prob = prob;
+  S->ctx = ctx;
+  S->opt = *opt;
+  if (S->opt.timing || (ctx->comm && !ctx->comm->capturable())) S->opt.use_graph = 0;
+  if (S->opt.newton_mode == 1) S->opt.use_graph = 0;
+  S->G = G;
+  S->n = 3 * G;
+  S->nglobal = y0->global_len;
+  int64_t n = S->n;
+  int e = 0;
+  for (int i = 0; i < 3 && !e; ++i) e = alloc(S, &S->y[i], n);
+  for (int i = 0; i < 2 && !e; ++i) e = alloc(S, &S->fE[i], n);
+  if (!e && !opt->fused) {
+    e = alloc(S, &S->d, n);
+    if (!e) e = alloc(S, &S->ewt, n);
+    if (!e) e = alloc(S, &S->tmp, n);
+    if (!e) e = alloc(S, &S->fI, n);
+    if (!e) e = alloc(S, &S->r, n);
+    if (!e) e = alloc(S, &S->delta, n);
+    if (!e) e = alloc(S, &S->M, 9 * G);
+    if (!e && cudaMalloc(&S->piv, sizeof(int32_t) * (G > 0 ? G : 1)) != cudaSuccess) e = SUNBW_ERR_MEM;
+  }
+  if (!e) e = alloc(S, &S->d_scal, kMaxK + 8);
+  if (!e) e = alloc(S, &S->d_partials, (int64_t)(ctx->nsm * 16) * (kMaxK + 1));
+  if (!e && cudaMalloc(&S->d_first, sizeof(unsigned long long)) != cudaSuccess) e = SUNBW_ERR_MEM;
+  if (!e && cudaMalloc(&S->d_err, sizeof(int)) != cudaSuccess) e = SUNBW_ERR_MEM;
+  if (e) {
+    cudaGetLastError();
+    BW_StepperDestroy(S);
+    return ctx_set_err(ctx, e);
+  }
+  if (cudaMemcpyAsync(S->y[S->iy], y0->d, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(S->d_first, 0xFF, sizeof(unsigned long long), ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(S->d_err, 0, sizeof(int), ctx->stream) != cudaSuccess) {
+    BW_StepperDestroy(S);
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  }
+  *out = S;
+  return 0;
+}
+
+extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, BW_StepperStats* stats) {
+  auto* S = (Stepper*)stepper;
+  if (!S || nsteps < 0) return SUNBW_ERR_ARG;
+  SUNBW_Context ctx = S->ctx;
+  if (y_out && (y_out->ctx != ctx || y_out->local_len != S->n)) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
+  int rc = 0;
+  for (int64_t s = 0; s < nsteps; ++s) {
+    bool first = S->step == 0;
+    if (S->opt.use_graph && !first) {
+      int key = graph_key(S);
+      if (!S->gexec[key]) {
+        int e = capture_step(S, key);
+        if (e) return e;
+      }
+      if (cudaGraphLaunch(S->gexec[key], ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      ctx->launches += S->graph_launches[key];
+      S->st.newton_iters += S->opt.K;
+      S->st.solves += S->opt.fused ? 0 : S->opt.K;
+    } else {
+      int64_t it0 = S->st.newton_iters;
+      rc = enqueue_step(S, first);
+      if (S->opt.fused) S->st.newton_iters = it0 + S->opt.K;
+      if (rc < 0) return rc;
+      if (rc > 0) { S->st.fails++; break; }
+    }
+    S->st.setups++;
+    rotate(S);
+    S->step++;
+    S->t += S->opt.h;
+    S->st.steps++;
+  }
+  // end of the call: one synchronisation for the deferred checks
+  unsigned long long f = 0;
+  int err = 0;
+  double nu = 0.0;
+  if (S->opt.newton_mode == 0) {
+    if (cudaMemcpyAsync(&f, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(&err, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(&nu, S->d_scal + S->opt.K, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+      return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  }
+  if (y_out &&
+      cudaMemcpyAsync(y_out->d, S->y[S->iy], sizeof(double) * S->n, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  if (S->opt.timing) harvest_timing(S);
+  if (S->opt.newton_mode == 0 && nsteps > 0) {
+    S->st.last_nu = nu;
+    if (f != ~0ull) { S->st.singular = (int64_t)f; rc = rc ? rc : SUNBW_RECOV_SINGULAR; }
+    if (err) rc = rc ? rc : SUNBW_RECOV_BAD_EWT;
+  }
+  S->st.t = S->t;
+  if (stats) *stats = S->st;
+  return rc;
+}
+
+extern "C" int BW_StepperReset(void* stepper, N_Vector y0, double t0) {
+  auto* S = (Stepper*)stepper;
+  if (!S || !y0) return SUNBW_ERR_ARG;
+  SUNBW_Context ctx = S->ctx;
+  if (y0->ctx != ctx || y0->local_len != S->n) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
+  S->iy = 0; S->iyp = 1; S->iz = 2; S->ife = 0; S->ifep = 1;   // graphs stay valid per key
+  if (cudaMemcpyAsync(S->y[S->iy], y0->d, sizeof(double) * S->n, cudaMemcpyDeviceToDevice,
+                      ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(S->d_first, 0xFF, sizeof(unsigned long long), ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(S->d_err, 0, sizeof(int), ctx->stream) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  S->step = 0;
+  S->t = t0;
+  S->st = BW_StepperStats{};
+  return 0;
+}
+
+extern "C" int BW_StepperKernelTimes(void* stepper, double* ms, int64_t* launches, int reset) {
+  auto* S = (Stepper*)stepper;
+  if (!S) return SUNBW_ERR_ARG;
+  for (int k = 0; k < BW_K_COUNT_; ++k) {
+    if (ms) ms[k] = S->k_ms[k];
+    if (launches) launches[k] = S->k_count[k];
+    if (reset) { S->k_ms[k] = 0; S->k_count[k] = 0; }
+  }
+  return 0;
+}
+
+extern "C" int BW_StepperDestroy(void* stepper) {
+  auto* S = (Stepper*)stepper;
+  if (!S) return SUNBW_ERR_ARG;
+  cudaStreamSynchronize(S->ctx->stream);
+  for (auto& g : S->gexec)
+    if (g) cudaGraphExecDestroy(g);
+  if (S->cap_stream) cudaStreamDestroy(S->cap_stream);
+  for (auto e : S->ev_pool) cudaEventDestroy(e);
+  double* bufs[] = {S->y[0], S->y[1], S->y[2], S->fE[0], S->fE[1], S->d, S->ewt, S->tmp,
+                    S->fI, S->r, S->delta, S->M, S->d_scal, S->d_partials};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  if (S->piv) cudaFree(S->piv);
+  if (S->d_first) cudaFree(S->d_first);
+  if (S->d_err) cudaFree(S->d_err);
+  delete S;
+  return 0;
+}

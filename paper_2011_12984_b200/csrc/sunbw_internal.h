@@ -1,0 +1,142 @@
+// sunbw_internal.h — private declarations shared by the libsunbw sources.
+// (Never included by the oracle; the oracle shares nothing with this tree.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
+#include <vector>
+
+#include "sunbw.h"
+
+#define SUNBW_MAX_SM 256
+
+// ------------------------------------------------------------ communicator
+enum RedOp { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
+
+struct Comm {
+  int rank = 0, nranks = 1;
+  virtual ~Comm() {}
+  // in-place allreduce of `count` doubles in device memory, on stream s
+  virtual int allreduce(double* d_buf, int count, RedOp op, cudaStream_t s) = 0;
+  // ring shift: send `count` doubles to rank+1, receive from rank-1
+  virtual int halo_shift(const double* d_send, double* d_recv, size_t count,
+                         cudaStream_t s) = 0;
+  virtual bool capturable() const = 0;   // may run inside CUDA graph capture
+};
+
+Comm* make_nccl_comm(const void* uid, int rank, int nranks, int* err);
+Comm* make_fake_comm_member(void* shared, int rank, int* err);
+
+// ----------------------------------------------------------------- context
+struct SUNBW_Context_ {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nsm = 148;
+  int err = 0;                          // sticky error
+  std::atomic<int64_t> launches{0};
+  Comm* comm = nullptr;                 // nullptr: single rank
+  // reduction scratch (stable addresses: usable inside graph capture)
+  double* d_partials = nullptr;         // kPartialsCap doubles
+  double* d_red = nullptr;              // kRedSlots doubles (device results)
+  double* h_slot = nullptr;             // pinned-mapped host slot
+  double* h_slot_dev = nullptr;         // its device alias
+  unsigned long long* d_flag = nullptr; // LU singular-block min
+  static constexpr int kPartialsCap = 1 << 16;
+  static constexpr int kRedSlots = 256;
+};
+
+int  ctx_set_err(SUNBW_Context ctx, int code);
+int  ctx_check_launch(SUNBW_Context ctx);   // cudaGetLastError -> sticky
+inline int ctx_rank(SUNBW_Context c) { return c->comm ? c->comm->rank : 0; }
+inline int ctx_nranks(SUNBW_Context c) { return c->comm ? c->comm->nranks : 1; }
+
+// ---------------------------------------------------------------- N_Vector
+struct _N_Vector {
+  SUNBW_Context ctx;
+  int64_t local_len;
+  int64_t global_len;
+  double* d;
+  bool owned;
+  int policy = SUNBW_POLICY_GRID_STRIDE;
+  int block = 256;
+  int grid = 0;
+  int reduce_block = 256;
+};
+
+// ---------------------------------------------------------- block matrix
+struct _SUNMatrix {
+  SUNBW_Context ctx;
+  int64_t nblocks;
+  int m;
+  double* d;
+  bool owned;
+};
+
+struct _SUNLinearSolver {
+  SUNBW_Context ctx;
+  int64_t nblocks;
+  int m;
+  int32_t* d_piv;
+  int deferred = 0;
+  int64_t last_flag = 0;
+  bool flag_pending = false;
+};
+
+// ------------------------------------------- internal (device-result) API
+// Launch-level entry points used by the driver; they never synchronise.
+// Results land in device memory so that a step can be graph-captured.
+namespace sunbw {
+
+struct LaunchCfg {
+  int block;
+  int grid;
+};
+
+// streaming
+int linear_sum(SUNBW_Context, int64_t n, double a, const double* x, double b,
+               const double* y, double* z, const _N_Vector* pol);
+int scale(SUNBW_Context, int64_t n, double c, const double* x, double* z,
+          const _N_Vector* pol);
+int abs_(SUNBW_Context, int64_t n, const double* x, double* z, const _N_Vector* pol);
+int add_const(SUNBW_Context, int64_t n, const double* x, double b, double* z,
+              const _N_Vector* pol);
+int inv(SUNBW_Context, int64_t n, const double* x, double* z, const _N_Vector* pol);
+// fused z = Σ c_j X_j (nv any)
+int linear_combination(SUNBW_Context, int64_t n, int nv, const double* c,
+                       const double* const* X, double* z, const _N_Vector* pol);
+
+// reductions.  kind: see RedKind.  Writes the GLOBAL result (after the
+// communicator's allreduce and the finalisation) to d_out[0..nv) and, if
+// h_out_dev != nullptr, also to that (mapped host) address.
+enum RedKind { RK_DOT = 0, RK_WSQR = 1, RK_WSQR_MASK = 2, RK_MAXABS = 3, RK_MIN = 4 };
+enum RedFinal { RF_NONE = 0, RF_WRMS = 1 };
+int reduce(SUNBW_Context, RedKind kind, RedFinal fin, int64_t n_local,
+           int64_t n_global, const double* x, const double* y, const double* id,
+           double* d_out, double* h_out_dev, bool global, const _N_Vector* pol);
+int dot_multi(SUNBW_Context, int64_t n_local, int nv, const double* x,
+              const double* const* Y, double* d_out, double* h_out_dev,
+              bool global, const _N_Vector* pol);
+
+// kernel: d_flag |= (d_val[0] <= 0) for the ewt check
+int flag_nonpositive(SUNBW_Context, const double* d_val, int* d_flag);
+
+// block diagonal
+int scale_add_identity(SUNBW_Context, int64_t G, int m, double c, double* A);
+int lu_factor(SUNBW_Context, int64_t G, int m, double* A, int32_t* piv,
+              unsigned long long* d_first_singular);
+int lu_solve(SUNBW_Context, int64_t G, int m, const double* LU,
+             const int32_t* piv, const double* b, double* x);
+int block_matvec(SUNBW_Context, int64_t G, int m, const double* A,
+                 const double* x, double* y);
+
+}  // namespace sunbw
+
+#define SUNBW_CUDA_TRY(ctx, expr)                                \
+  do {                                                           \
+    cudaError_t e_ = (expr);                                     \
+    if (e_ != cudaSuccess) return ctx_set_err((ctx), SUNBW_ERR_CUDA); \
+  } while (0)

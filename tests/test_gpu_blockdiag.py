@@ -1,0 +1,120 @@
+"""GPU parity of the block-diagonal matrix and batched LU (through the C ABI)
+against the oracle: factors, pivots and solutions bit-exact (same RN
+operation order, no contraction); singular-block flag exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import assert_bits_equal, needs_cuda
+
+pytestmark = [pytest.mark.gpu, needs_cuda]
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2011_12984_b200 import sunbw
+    return sunbw
+
+
+@pytest.fixture(scope="module")
+def ctx(S):
+    c = S.Context(0)
+    yield c
+    c.destroy()
+
+
+def blocks(stream, G, m, diag=0.0):
+    A = synth.uniform(stream, G * m * m, -1, 1).reshape(G, m, m)
+    return A + diag * torch.eye(m, dtype=torch.float64)
+
+
+def decode(code, m):
+    code = code.numpy().astype(np.int64)
+    return np.stack([(code >> (3 * k)) & 7 for k in range(m)], axis=1).astype(np.int32)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("G", [1, 31, 129, 1000, 70001])
+def test_factor_solve_bit_exact(S, ctx, m, G):
+    A = blocks(40 + m, G, m, diag=0.5)
+    Ad = A.cuda().contiguous()
+    M = S.SUNMatrix(ctx, Ad)
+    b = synth.uniform(50, G * m, -1, 1).cuda()
+    x = torch.empty_like(b)
+    vb, vx = S.NVector(ctx, b), S.NVector(ctx, x)
+    LS = S.SUNLinearSolver(vb, M)
+    assert S.SUNLinSolSetup(LS, M) == 0
+    LU, piv, flag = oracle.lu_factor(A.numpy())
+    assert flag == 0 and S.SUNLinSolLastFlag(LS) == 0
+    assert_bits_equal(Ad.reshape(-1), LU.reshape(-1), f"LU m={m} G={G}")
+    assert np.array_equal(decode(LS.pivots(), m), piv)
+    S.SUNLinSolSolve(LS, M, vx, vb)
+    ctx.check("solve")
+    assert_bits_equal(x, oracle.lu_solve(LU, piv, b.cpu().numpy()), f"solve m={m} G={G}")
+    # in place x == b
+    S.SUNLinSolSolve(LS, M, vb, vb)
+    assert_bits_equal(b, x.cpu().numpy(), "solve in place")
+
+
+def test_pivot_forcing_permutation_and_singular(S, ctx):
+    G = 300
+    A = blocks(60, G, 3)
+    A[::3] = A[::3][:, [2, 0, 1]] * torch.tensor([1e-3, 1.0, 1.0], dtype=torch.float64)[:, None]
+    perm = torch.tensor([[0, 1, 0], [0, 0, 1], [1, 0, 0]], dtype=torch.float64)
+    A[5] = perm
+    A[17, :, 1] = 0.0           # exactly zero pivot in column 1
+    A[200] = 0.0
+    Ad = A.cuda().contiguous()
+    M = S.SUNMatrix(ctx, Ad)
+    b = synth.uniform(61, G * 3, -1, 1).cuda()
+    LS = S.SUNLinearSolver(S.NVector(ctx, b), M)
+    assert S.SUNLinSolSetup(LS, M) == 1                   # SUNBW_RECOV_SINGULAR
+    assert S.SUNLinSolLastFlag(LS) == 18                  # 1 + first singular block
+    LU, piv, flag = oracle.lu_factor(A.numpy())
+    assert flag == 18
+    assert_bits_equal(Ad.reshape(-1), LU.reshape(-1), "LU with singular blocks")
+    assert np.array_equal(decode(LS.pivots(), 3), piv)
+    # deferred check: Setup returns 0, the flag is read later
+    Ad.copy_(A.cuda())
+    S.SUNLinSol_B200BatchedLU_SetDeferredCheck(LS, True)
+    assert S.SUNLinSolSetup(LS, M) == 0
+    assert S.SUNLinSolLastFlag(LS) == 18
+
+
+def test_scale_add_identity_and_matvec(S, ctx):
+    for m, G in [(3, 10001), (5, 777), (1, 33)]:
+        A = blocks(70, G, m)
+        Ad = A.cuda().contiguous()
+        M = S.SUNMatrix(ctx, Ad)
+        S.SUNMatScaleAddI(-0.37, M)
+        ref = oracle.scale_add_identity(-0.37, A.numpy())
+        assert_bits_equal(Ad.reshape(-1), ref.reshape(-1), f"ScaleAddI m={m}")
+        x = synth.uniform(71, G * m, -1, 1).cuda()
+        y = torch.empty_like(x)
+        S.SUNMatMatvec(M, S.NVector(ctx, x), S.NVector(ctx, y))
+        assert_bits_equal(y, oracle.block_matvec(ref, x.cpu().numpy()), f"matvec m={m}")
+
+
+def test_newton_matrix_from_jacobian(S, ctx):
+    """M = I - γ J(y) for the Brusselator: Jacobian + ScaleAddI + Setup,
+    the C4 Setup path, against the oracle."""
+    G = 50_001
+    y = torch.stack([synth.uniform(1, G, 0.5, 2), synth.uniform(2, G, 0.5, 4),
+                     synth.uniform(3, G, 0.5, 4)], 1).reshape(-1).cuda()
+    P = S.Problem(ctx, S.bruss_params(dim=1, nx=G, reaction_only=True))
+    Jd = torch.empty(G, 3, 3, dtype=torch.float64, device="cuda")
+    M = S.SUNMatrix(ctx, Jd)
+    S.BW_ReactionJacobian(P, S.NVector(ctx, y), M)
+    Jref = oracle.bruss_jacobian(y.cpu().numpy())
+    assert_bits_equal(Jd.reshape(-1), Jref.reshape(-1), "Jacobian")
+    gamma = 2e-3 / 3
+    S.SUNMatScaleAddI(-gamma, M)
+    Mref = oracle.scale_add_identity(-gamma, Jref)
+    assert_bits_equal(Jd.reshape(-1), Mref.reshape(-1), "M")
+    LS = S.SUNLinearSolver(S.NVector(ctx, y), M)
+    assert S.SUNLinSolSetup(LS, M) == 0
+    LU, piv, _ = oracle.lu_factor(Mref)
+    assert_bits_equal(Jd.reshape(-1), LU.reshape(-1), "LU(M)")
+    P.destroy()
