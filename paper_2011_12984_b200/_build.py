@@ -39,17 +39,22 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile and link libsunbw.so.  `defines` (e.g. ["SUNBW_FUSED_MINB=8"])
+    and `out` build a tuning variant elsewhere (build/var_*/libsunbw.so)."""
     nccl = nccl_dir()
-    os.makedirs(OBJDIR, exist_ok=True)
+    lib = out or LIB
+    objdir = OBJDIR if not defines else os.path.join(os.path.dirname(lib), "obj")
+    os.makedirs(objdir, exist_ok=True)
+    dflags = ["-D" + d for d in defines]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "sunbw.h")]
     incs = ["-I" + INCLUDE, "-I" + os.path.join(nccl, "include")]
 
     def compile_one(src):
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + hdrs):
-            cmd = ["nvcc", *ARCH, *NVCCFLAGS, *incs, "-c", s, "-o", o]
+            cmd = ["nvcc", *ARCH, *NVCCFLAGS, *dflags, *incs, "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             r = subprocess.run(cmd, capture_output=True, text=True)
@@ -59,14 +64,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    if force or _stale(LIB, objs):
+    if force or _stale(lib, objs):
         libdir = os.path.join(nccl, "lib")
-        cmd = ["nvcc", *ARCH, "-shared", "-o", LIB, *objs, "-L" + libdir, "-l:libnccl.so.2",
+        cmd = ["nvcc", *ARCH, "-shared", "-o", lib, *objs, "-L" + libdir, "-l:libnccl.so.2",
                "-Xlinker", "-rpath," + libdir]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

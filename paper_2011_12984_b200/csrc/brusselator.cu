@@ -17,6 +17,7 @@
 
 #include <cmath>
 
+#include "sunbw_device.cuh"
 #include "sunbw_internal.h"
 
 namespace {
@@ -197,6 +198,54 @@ __global__ void __launch_bounds__(256) k_adv3d(const double* __restrict__ y,
   }
 }
 
+// Vectorised 3D variant for 3·nx % 4 == 0 (nx % 4 == 0) and 32-B aligned
+// rows: thread v owns the 4 values [4v, 4v+4) of the row; the row is staged
+// in shared memory for the x-neighbour (e-3 crosses 32-B vectors), the y-1
+// row and the z-1 plane row are read as aligned 256-bit vectors (they are
+// L2 hits: the row below was read ~one plane earlier).  Same arithmetic and
+// order as k_adv3d.
+__global__ void __launch_bounds__(256) k_adv3d_v4(const double* __restrict__ y,
+                                                  const double* __restrict__ below,
+                                                  double* __restrict__ f, Adv3 a) {
+  __shared__ __align__(32) double srow[3 * 1024];
+  const int rowlen = 3 * a.nx;
+  const int nv = rowlen / 4;
+  const int64_t plane = (int64_t)rowlen * a.ny;
+  const int nrows = a.ny * a.nzl;
+  for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const int j = r % a.ny, k = r / a.ny;
+    const int64_t base = (int64_t)r * rowlen;
+    const double* yrow = y + base;
+    const double* ym = j > 0 ? yrow - rowlen : yrow + (int64_t)(a.ny - 1) * rowlen;
+    const double* zm = k > 0 ? yrow - plane : below + (int64_t)j * rowlen;
+    __syncthreads();
+    sunbw::d4 q[2], qy[2], qz[2];
+    int cnt = 0;
+    for (int v = threadIdx.x; v < nv && cnt < 2; v += blockDim.x, ++cnt) {
+      q[cnt] = sunbw::ld4(yrow + 4 * v);
+      if (a.ny_g > 1) qy[cnt] = sunbw::ld4(ym + 4 * v);
+      if (a.nz_g > 1) qz[cnt] = sunbw::ld4(zm + 4 * v);
+      *reinterpret_cast<sunbw::d4*>(srow + 4 * v) = q[cnt];
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int v = threadIdx.x; v < nv && cnt < 2; v += blockDim.x, ++cnt) {
+      sunbw::d4 o;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const int e = 4 * v + l;
+        const double qq = q[cnt].v[l];
+        const double qx = srow[e >= 3 ? e - 3 : e + rowlen - 3];
+        double acc = __dmul_rn(a.kx, __dsub_rn(qx, qq));
+        if (a.ny_g > 1) acc = __dadd_rn(acc, __dmul_rn(a.ky, __dsub_rn(qy[cnt].v[l], qq)));
+        if (a.nz_g > 1) acc = __dadd_rn(acc, __dmul_rn(a.kz, __dsub_rn(qz[cnt].v[l], qq)));
+        o.v[l] = acc;
+      }
+      sunbw::st4(f + base + 4 * v, o);
+    }
+  }
+}
+
 int grid_cells(SUNBW_Context ctx, int64_t G) {
   int64_t need = (G + kCells - 1) / kCells;
   int64_t cap = (int64_t)ctx->nsm * 16;
@@ -271,7 +320,21 @@ int bw_advection_stencil(void* prob, const double* y, double* f) {
   } else {
     Adv3 a{(int)P->nxl, (int)P->nyl, (int)P->nzl, (int)P->p.ny, (int)P->p.nz, P->kx, P->ky, P->kz};
     int rows = (int)(P->nyl * P->nzl);
-    k_adv3d<<<rows, 256, 0, ctx->stream>>>(y, left, f, a);
+    const int rowlen = 3 * (int)P->nxl;
+#ifndef SUNBW_ADV_VARIANT
+#define SUNBW_ADV_VARIANT 0   // 0: per-element kernel (fastest measured); 1/2: vectorised
+#endif
+    const bool vec = SUNBW_ADV_VARIANT > 0 && rowlen % 4 == 0 && rowlen <= 2048 &&
+                     (((uintptr_t)y | (uintptr_t)f | (uintptr_t)left) & 31) == 0;
+    if (vec) {
+      int nv = rowlen / 4;
+      int block = nv <= 256 ? ((nv + 31) / 32) * 32 : 256;
+      int64_t cap = SUNBW_ADV_VARIANT == 1 ? (int64_t)ctx->nsm * (2048 / block) : rows;
+      int grid = (int)(rows < cap ? rows : cap);
+      k_adv3d_v4<<<grid, block, 0, ctx->stream>>>(y, left, f, a);
+    } else {
+      k_adv3d<<<rows, 256, 0, ctx->stream>>>(y, left, f, a);
+    }
   }
   ctx->launches++;
   return ctx_check_launch(ctx);

@@ -16,7 +16,7 @@ from typing import Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsunbw.so")
+LIB_PATH = os.environ.get("SUNBW_LIB", os.path.join(_HERE, "libsunbw.so"))
 
 _lib = None
 _P = C.c_void_p
