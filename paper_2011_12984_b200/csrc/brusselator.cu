@@ -343,6 +343,21 @@ int bw_advection_stencil(void* prob, const double* y, double* f) {
 int64_t bw_local_cells(void* prob) { return ((Prob*)prob)->G; }
 BW_BrussParams bw_params(void* prob) { return ((Prob*)prob)->p; }
 
+bool bw_fused_advection(void* prob, const double* y, FusedAdvection* fa) {
+  auto* P = (Prob*)prob;
+  const BW_BrussParams& p = P->p;
+  if (p.dim != 3 || p.kind != 0 || p.reaction_only || P->nxl % 128 != 0 || p.ny < 2 || p.nz < 2)
+    return false;
+  fa->nx = P->nxl;
+  fa->ny = P->nyl;
+  fa->nzl = P->nzl;
+  fa->kx = P->kx;
+  fa->ky = P->ky;
+  fa->kz = P->kz;
+  fa->below = ctx_nranks(P->ctx) > 1 ? P->d_halo : y + 3 * P->G - P->halo_len;
+  return true;
+}
+
 }  // namespace sunbw
 
 // ==================================================================== C ABI

@@ -43,7 +43,7 @@ int lu_factor_noreset(SUNBW_Context, int64_t G, int m, double* A, int32_t* piv,
 int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, double h,
                  double rtol, double atol, const double* y, const double* yp, const double* fE,
                  const double* fEp, double* z, double* partials, unsigned long long* d_first,
-                 int* nblocks_out);
+                 int* nblocks_out, const FusedAdvection* adv);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
                double* d_min, double* d_nu, int* d_err);
 }  // namespace sunbw
@@ -146,14 +146,22 @@ int enqueue_step(Stepper* S, bool first) {
   const double gamma = first ? h : (2.0 * h) / 3.0;
 
   { Timed t(S, BW_K_HALO); TRY(sunbw::bw_halo(S->prob, y)); }
-  { Timed t(S, BW_K_ADVECTION); TRY(sunbw::bw_advection_stencil(S->prob, y, fE)); }
+  sunbw::FusedAdvection fa;
+  const bool adv_in_kernel = o.fused && o.fused_advection && sunbw::bw_fused_advection(S->prob, y, &fa) &&
+                             G % 128 == 0;
+  if (!adv_in_kernel) {
+    Timed t(S, BW_K_ADVECTION);
+    TRY(sunbw::bw_advection_stencil(S->prob, y, fE));
+  }
 
   if (o.fused) {
     int nb = 0;
     {
+      // with in-kernel advection fE is the f_E,n output (kept for the next
+      // step's f_E,n-1), otherwise the input computed above
       Timed t(S, BW_K_FUSED_NEWTON);
       TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
-                              S->d_partials, S->d_first, &nb));
+                              S->d_partials, S->d_first, &nb, adv_in_kernel ? &fa : nullptr));
     }
     { Timed t(S, BW_K_WRMS); TRY(sunbw::fused_fold(ctx, S->d_partials, nb, o.K, S->nglobal, S->d_scal,
                                                   S->d_scal + 1, S->d_err)); }

@@ -133,6 +133,16 @@ int lu_solve(SUNBW_Context, int64_t G, int m, const double* LU,
 int block_matvec(SUNBW_Context, int64_t G, int m, const double* A,
                  const double* x, double* y);
 
+// geometry for the fused step kernel's in-kernel 3D advection
+struct FusedAdvection {
+  int64_t nx, ny, nzl;       // local slab extents (nx % 128 == 0)
+  double kx, ky, kz;
+  const double* below;       // the plane under local plane 0 (halo or own last)
+};
+// fills *fa and returns true when the problem's advection can be fused into
+// the Newton kernel (3D Brusselator, nx % 128 == 0, ny > 1, nz > 1)
+bool bw_fused_advection(void* prob, const double* y, FusedAdvection* fa);
+
 }  // namespace sunbw
 
 #define SUNBW_CUDA_TRY(ctx, expr)                                \

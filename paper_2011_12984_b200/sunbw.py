@@ -44,7 +44,7 @@ class BW_BrussParams(C.Structure):
 class BW_StepperOptions(C.Structure):
     _fields_ = [("h", _D), ("newton_mode", C.c_int32), ("K", C.c_int32), ("tol_nl", _D),
                 ("rtol", _D), ("atol", _D), ("use_graph", C.c_int32), ("timing", C.c_int32),
-                ("fused", C.c_int32), ("pad_", C.c_int32)]
+                ("fused", C.c_int32), ("fused_advection", C.c_int32)]
 
 
 class BW_StepperStats(C.Structure):
@@ -453,9 +453,10 @@ def BW_ReactionJacobian(P: Problem, y: NVector, J: SUNMatrix) -> int:
 
 
 def stepper_options(h=1e-3, newton_mode=0, K=3, tol_nl=1e-3, rtol=1e-6, atol=1e-9,
-                    use_graph=True, timing=False, fused=False) -> BW_StepperOptions:
+                    use_graph=True, timing=False, fused=False,
+                    fused_advection=True) -> BW_StepperOptions:
     return BW_StepperOptions(h, newton_mode, K, tol_nl, rtol, atol, int(use_graph), int(timing),
-                             int(fused), 0)
+                             int(fused), int(fused_advection))
 
 
 class Stepper:

@@ -149,6 +149,25 @@ def test_3D_small_matches_oracle(S, ctx):
         assert_bits_equal(y, yref, f"3D fused={fused}")
 
 
+@pytest.mark.parametrize("shape", [(128, 6, 4), (256, 4, 3), (128, 3, 2)])
+@pytest.mark.parametrize("fused_adv", [True, False])
+def test_3D_fused_step_kernel(S, ctx, shape, fused_adv):
+    """The single-kernel step (advection inside the TMA-staged Newton
+    kernel, nx % 128 == 0) against the oracle, SBDF1 + SBDF2 steps."""
+    nx, ny, nz = shape
+    steps = 6
+    y0 = oracle.bruss_ic(nx, ny, nz)
+    k = kappas(nx, ny, nz)
+    _, yref, stref, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=nx, ny=ny, nz=nz,
+                                              kx=k[0], ky=k[1], kz=k[2], h=1e-3)
+    params = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz)
+    rc, y, stats = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=True,
+                           fused_advection=fused_adv, use_graph=True)
+    assert rc == 0
+    assert_bits_equal(y, yref, f"fused step {shape} adv={fused_adv}")
+    assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-9 * stref["last_nu"]
+
+
 def test_tolerance_mode(S, ctx):
     nx, steps = 64, 50
     y0 = oracle.bruss_ic(nx)
@@ -210,10 +229,12 @@ def run_ranks(S, nranks, fn):
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
-@pytest.mark.parametrize("dim", [1, 3])
-def test_multirank_driver_invariance(S, nranks, dim):
+@pytest.mark.parametrize("dim,fused", [(1, False), (3, False), (3, True), ("3big", True)])
+def test_multirank_driver_invariance(S, nranks, dim, fused):
     if dim == 1:
         shape = (96, 1, 1)
+    elif dim == "3big":
+        shape, dim = (128, 4, 8), 3          # in-kernel advection, halo plane via TMA
     else:
         shape = (12, 10, 8)
     nx, ny, nz = shape
@@ -230,7 +251,8 @@ def test_multirank_driver_invariance(S, nranks, dim):
         off = 3 * P.cell_offset
         y = torch.from_numpy(y0[off:off + n].copy()).cuda()
         yout = torch.empty_like(y)
-        st = S.Stepper(P, S.NVector(c, y), S.stepper_options(h=1e-3, K=3, use_graph=False))
+        st = S.Stepper(P, S.NVector(c, y), S.stepper_options(h=1e-3, K=3, use_graph=False,
+                                                              fused=fused))
         rc, stats = st.advance(steps, S.NVector(c, yout))
         c.stream.synchronize()
         res = (rc, off, yout.cpu().numpy(), stats)
