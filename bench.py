@@ -114,6 +114,28 @@ def dist_setup(n_gpus):
     return world, rank, local
 
 
+def slab(rank: int, world: int, n_ax: int):
+    """z-slab of rank `rank` in the weak-scaled C5 grid (n_ax^2 x n_ax*world):
+    (first global plane, local planes, domain length Lz) — MPIPlusX layout."""
+    return rank * n_ax, n_ax, float(world)
+
+
+def broadcast_uid(uid, rank: int, dist):
+    """NCCL unique id from rank 0 to every rank through the torch store."""
+    box = [uid if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
+def max_over_ranks(ms: float, dist, world: int, device) -> float:
+    """The job time is the slowest rank's (device-timed) time."""
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_reference(args, world, rank):
     """The serial CPU oracle, as it stands, on a bounded sample of the same
     workload: a 256 x 256 x nzs slab (periodic), same parameters, fixed K."""
@@ -152,7 +174,7 @@ METRIC = ("advection-reaction throughput, cell time-steps/s (3D Brusselator, 256
           "SBDF2 + K=3 block-LU Newton, fp64)")
 
 
-def cpu_baseline_sample(planes=64, steps=6):
+def cpu_baseline_sample(planes=64, steps=15):
     """Oracle on the GPU box's host, one core, bounded sample (~10 s)."""
     import oracle
     oracle.build()
@@ -238,13 +260,13 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = S.Context(local)
     if world > 1:
-        uid = [S.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.init_nccl(uid[0], rank, world)
+        uid = broadcast_uid(S.nccl_unique_id() if rank == 0 else None, rank, dist)
+        ctx.init_nccl(uid, rank, world)
 
     n_ax = args.cells
     G = n_ax ** 3
-    params = S.bruss_params(dim=3, nx=n_ax, ny=n_ax, nz=n_ax * world, Lx=1.0, Ly=1.0, Lz=float(world))
+    z0, nzl, Lz = slab(rank, world, n_ax)
+    params = S.bruss_params(dim=3, nx=n_ax, ny=n_ax, nz=n_ax * world, Lx=1.0, Ly=1.0, Lz=Lz)
     P = S.Problem(ctx, params)
     assert P.local_cells == G
     y0 = torch.empty(3 * G, dtype=torch.float64, device="cuda")
@@ -279,10 +301,7 @@ def main():
     launches = ctx.launches - l0
     assert rc == 0, rc
     ms_local = e0.elapsed_time(e1)
-    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_over_ranks(ms_local, dist, world, "cuda")
     value = world * G * args.steps / (ms * 1e-3)
 
     # per-kernel device times inside the timed region (CUDA events on the
@@ -327,10 +346,7 @@ def main():
     host_out.copy_(yout, non_blocking=True)
     f1.record(stream)
     torch.cuda.synchronize()
-    te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1), dist, world, "cuda")
     state_bytes = 3 * G * 8
     e2e = {"value": world * G * args.steps / (e2e_ms * 1e-3), "unit": "cell-steps/s",
            "h2d_bytes_per_step": state_bytes / args.steps, "d2h_bytes_per_step": state_bytes / args.steps,
