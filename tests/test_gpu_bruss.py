@@ -290,3 +290,38 @@ def test_multirank_reductions(S, nranks):
     assert abs(dt - oracle.dot(x, w)) <= 1e-12 * float(np.sum(np.abs(x * w)))
     assert mx == oracle.max_norm(x) and mn == oracle.min_(x)
     assert abs(dm[1] - oracle.dot(x, x)) <= 1e-12 * oracle.dot(x, x)
+
+
+# ------------------------------------------------ full bench-size parity
+@pytest.mark.slow
+@pytest.mark.parametrize("fused", [True, False])
+def test_C5_slab_full_size_two_steps(S, ctx, fused):
+    """The bench's workload and launch configuration (256^3 cells, fused
+    single-kernel step or the composed path), SBDF1 + SBDF2 steps, the whole
+    state against the oracle run on the host (about 15 s of CPU)."""
+    n = 256
+    steps = 2
+    y0 = oracle.bruss_ic(n, n, n)
+    k = kappas(n, n, n)
+    _, yref, stref, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=n, ny=n, nz=n,
+                                              kx=k[0], ky=k[1], kz=k[2], h=1e-3)
+    params = S.bruss_params(dim=3, nx=n, ny=n, nz=n)
+    rc, y, stats = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=fused, use_graph=False)
+    assert rc == 0
+    assert_bits_equal(y, yref, f"C5 256^3 fused={fused}")
+    assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-9 * stref["last_nu"]
+
+
+@pytest.mark.slow
+def test_C4_full_size_1e7_cells(S, ctx):
+    """C4: 1e7 independent reaction cells, batched block Newton only, at full
+    size, two steps, fused and composed, against the oracle."""
+    G, steps = 10_000_000, 2
+    u = synth.uniform(synth.S_CELL, G, 0, 1).numpy()
+    y0 = np.stack([1.0 + 0.1 * u, 3.5 + 0.1 * u, 3.0 + 0.1 * u], 1).reshape(-1)
+    _, yref, _, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=G, reaction_only=True, h=1e-3)
+    params = S.bruss_params(dim=1, nx=G, reaction_only=True)
+    for fused in (True, False):
+        rc, y, _ = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=fused)
+        assert rc == 0
+        assert_bits_equal(y, yref, f"C4 1e7 fused={fused}")
