@@ -17,6 +17,7 @@
 
 #include "sunbw_device.cuh"
 #include "sunbw_internal.h"
+#include "pipeline.cuh"
 
 namespace {
 
@@ -274,6 +275,113 @@ inline int grid_for(SUNBW_Context ctx, int64_t G, int B, int occ) {
   return g < 1 ? 1 : (int)g;
 }
 
+// ---- TMA-pipelined variants (pipeline.cuh): every operand tile of T
+// blocks is one bulk copy; persistent CTAs, double-buffered.  Used when all
+// operands are 16-B aligned (always for library-allocated storage).
+template <int M>
+__host__ __device__ constexpr int tpc() {
+  return M <= 4 ? 128 : 32;
+}
+constexpr int kStagesLU = 2;
+
+template <int M>
+__global__ void __launch_bounds__(tpc<M>()) k_lu_factor_tma(sunbw::pipe::IO<1, 2> io, int64_t G,
+                                                           unsigned long long* first_singular) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  sunbw::pipe::run<tpc<M>(), kStagesLU>(
+      io, G, smem, [&](int, int64_t g, const unsigned char** ip, unsigned char** op) {
+        const double* ain = reinterpret_cast<const double*>(ip[0]);
+        double a[M][M];
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+          for (int j = 0; j < M; ++j) a[i][j] = ain[i * M + j];
+        bool sing;
+        int code = lu_regs<M>(a, sing);
+        double* aout = reinterpret_cast<double*>(op[0]);
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+          for (int j = 0; j < M; ++j) aout[i * M + j] = a[i][j];
+        *reinterpret_cast<int32_t*>(op[1]) = code;
+        if (sing) atomicMin(first_singular, (unsigned long long)(g + 1));
+      });
+}
+
+template <int M>
+__global__ void __launch_bounds__(tpc<M>()) k_lu_solve_tma(sunbw::pipe::IO<3, 1> io, int64_t G) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  sunbw::pipe::run<tpc<M>(), kStagesLU>(
+      io, G, smem, [&](int, int64_t, const unsigned char** ip, unsigned char** op) {
+        const double* lu = reinterpret_cast<const double*>(ip[0]);
+        const int code = *reinterpret_cast<const int32_t*>(ip[1]);
+        const double* b = reinterpret_cast<const double*>(ip[2]);
+        double a[M][M], y[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          y[i] = b[i];
+#pragma unroll
+          for (int j = 0; j < M; ++j) a[i][j] = lu[i * M + j];
+        }
+        lu_solve_regs<M>(a, code, y);
+        double* x = reinterpret_cast<double*>(op[0]);
+#pragma unroll
+        for (int i = 0; i < M; ++i) x[i] = y[i];
+      });
+}
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// persistent grid: resident CTAs per SM from the shared-memory footprint
+inline int grid_tma(SUNBW_Context ctx, int64_t G, int T, int smem) {
+  int64_t need = (G + T - 1) / T;
+  int occ = (220 * 1024) / smem;
+  if (occ > 2048 / T) occ = 2048 / T;
+  if (occ < 1) occ = 1;
+  int64_t cap = (int64_t)ctx->nsm * occ;
+  int64_t g = need < cap ? need : cap;
+  return g < 1 ? 1 : (int)g;
+}
+
+template <int M>
+int launch_lu_factor(SUNBW_Context ctx, int64_t G, double* A, int32_t* piv, unsigned long long* d_first) {
+  constexpr int T = tpc<M>();
+  if (aligned16(A) && aligned16(piv)) {
+    sunbw::pipe::IO<1, 2> io{{(const unsigned char*)A}, {M * M * 8}, {(unsigned char*)A, (unsigned char*)piv},
+                             {M * M * 8, 4}};
+    const int smem = 128 + T * (kStagesLU * M * M * 8 + M * M * 8 + 4);
+    static bool attr = cudaFuncSetAttribute(k_lu_factor_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            smem) == cudaSuccess;
+    if (!attr) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    k_lu_factor_tma<M><<<grid_tma(ctx, G, T, smem), T, smem, ctx->stream>>>(io, G, d_first);
+  } else {
+    k_lu_factor<M><<<grid_for(ctx, G, bpc<M>(), 16), bpc<M>(), 0, ctx->stream>>>(A, piv, G, d_first);
+  }
+  ctx->launches++;
+  return ctx_check_launch(ctx);
+}
+
+template <int M>
+int launch_lu_solve(SUNBW_Context ctx, int64_t G, const double* LU, const int32_t* piv, const double* b,
+                    double* x) {
+  constexpr int T = tpc<M>();
+  if (aligned16(LU) && aligned16(piv) && aligned16(b) && aligned16(x)) {
+    sunbw::pipe::IO<3, 1> io{{(const unsigned char*)LU, (const unsigned char*)piv, (const unsigned char*)b},
+                             {M * M * 8, 4, M * 8},
+                             {(unsigned char*)x},
+                             {M * 8}};
+    const int smem = 128 + T * (kStagesLU * (M * M * 8 + 4 + M * 8) + M * 8);
+    static bool attr = cudaFuncSetAttribute(k_lu_solve_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            smem) == cudaSuccess;
+    if (!attr) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    k_lu_solve_tma<M><<<grid_tma(ctx, G, T, smem), T, smem, ctx->stream>>>(io, G);
+  } else {
+    k_lu_solve<M><<<grid_for(ctx, G, bpc<M>(), 16), bpc<M>(), 0, ctx->stream>>>(LU, piv, b, x, G);
+  }
+  ctx->launches++;
+  return ctx_check_launch(ctx);
+}
+
 }  // namespace
 
 // ============================================================ internal API
@@ -285,44 +393,33 @@ namespace sunbw {
     default: return ctx_set_err(ctx, SUNBW_ERR_UNSUPPORTED); \
   }
 
-// resident CTAs per SM for the staged kernels: enough 32-B requests in flight
+// resident CTAs per SM for the staged (non-TMA) kernels
 constexpr int kOccLU = 16;
+
+// factor in place; d_first accumulates the first singular block (min)
+int lu_factor_noreset(SUNBW_Context ctx, int64_t G, int m, double* A, int32_t* piv,
+                      unsigned long long* d_first) {
+  if (G <= 0) return 0;
+#define LUF(M) \
+  case M: return launch_lu_factor<M>(ctx, G, A, piv, d_first);
+  DISPATCH_M(m, LUF)
+#undef LUF
+}
 
 int lu_factor(SUNBW_Context ctx, int64_t G, int m, double* A, int32_t* piv,
               unsigned long long* d_first) {
   if (cudaMemsetAsync(d_first, 0xFF, sizeof(unsigned long long), ctx->stream) != cudaSuccess)
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-  if (G <= 0) return 0;
-#define LUF(M) \
-  case M: k_lu_factor<M><<<grid_for(ctx, G, bpc<M>(), kOccLU), bpc<M>(), 0, ctx->stream>>>(A, piv, G, d_first); break;
-  DISPATCH_M(m, LUF)
-#undef LUF
-  ctx->launches++;
-  return ctx_check_launch(ctx);
-}
-
-// as lu_factor, but accumulates into d_first across calls (the driver
-// checks it once per Advance)
-int lu_factor_noreset(SUNBW_Context ctx, int64_t G, int m, double* A, int32_t* piv,
-                      unsigned long long* d_first) {
-  if (G <= 0) return 0;
-#define LUF(M) \
-  case M: k_lu_factor<M><<<grid_for(ctx, G, bpc<M>(), kOccLU), bpc<M>(), 0, ctx->stream>>>(A, piv, G, d_first); break;
-  DISPATCH_M(m, LUF)
-#undef LUF
-  ctx->launches++;
-  return ctx_check_launch(ctx);
+  return lu_factor_noreset(ctx, G, m, A, piv, d_first);
 }
 
 int lu_solve(SUNBW_Context ctx, int64_t G, int m, const double* LU, const int32_t* piv,
              const double* b, double* x) {
   if (G <= 0) return 0;
 #define LUS(M) \
-  case M: k_lu_solve<M><<<grid_for(ctx, G, bpc<M>(), kOccLU), bpc<M>(), 0, ctx->stream>>>(LU, piv, b, x, G); break;
+  case M: return launch_lu_solve<M>(ctx, G, LU, piv, b, x);
   DISPATCH_M(m, LUS)
 #undef LUS
-  ctx->launches++;
-  return ctx_check_launch(ctx);
 }
 
 int block_matvec(SUNBW_Context ctx, int64_t G, int m, const double* A, const double* x, double* y) {

@@ -58,6 +58,37 @@ def test_factor_solve_bit_exact(S, ctx, m, G):
     assert_bits_equal(b, x.cpu().numpy(), "solve in place")
 
 
+@pytest.mark.parametrize("m", [3, 5])
+def test_misaligned_storage_fallback(S, ctx, m):
+    """Matrix / vectors only 8-B aligned: the non-TMA staged kernels run;
+    same bits as the oracle (and as the aligned TMA path)."""
+    G = 4099
+    A = blocks(45, G, m, diag=0.5)
+    buf = torch.empty(G * m * m + 1, dtype=torch.float64, device="cuda")
+    Ad = buf[1:].view(G, m, m)
+    Ad.copy_(A)
+    M = S.SUNMatrix(ctx, Ad)
+    bbuf = torch.empty(G * m + 1, dtype=torch.float64, device="cuda")
+    b = bbuf[1:]
+    b.copy_(synth.uniform(51, G * m, -1, 1))
+    x = torch.empty_like(b)
+    LS = S.SUNLinearSolver(S.NVector(ctx, b), M)
+    assert S.SUNLinSolSetup(LS, M) == 0
+    LU, piv, _ = oracle.lu_factor(A.numpy())
+    assert_bits_equal(Ad.reshape(-1), LU.reshape(-1), f"LU misaligned m={m}")
+    S.SUNLinSolSolve(LS, M, S.NVector(ctx, x), S.NVector(ctx, b))
+    assert_bits_equal(x, oracle.lu_solve(LU, piv, b.cpu().numpy()), f"solve misaligned m={m}")
+    y = synth.uniform(1, 3 * G, 0.5, 2)
+    ybuf = torch.empty(3 * G + 1, dtype=torch.float64, device="cuda")
+    yd = ybuf[1:]
+    yd.copy_(y)
+    P = S.Problem(ctx, S.bruss_params(dim=1, nx=G))
+    f = torch.empty_like(yd)
+    S.BW_ReactionRHS(P, S.NVector(ctx, yd), S.NVector(ctx, f))
+    assert_bits_equal(f, oracle.bruss_reaction(y.numpy()), "reaction misaligned")
+    P.destroy()
+
+
 def test_pivot_forcing_permutation_and_singular(S, ctx):
     G = 300
     A = blocks(60, G, 3)
