@@ -70,6 +70,7 @@ _SIGS = {
     "SUNBW_ContextSetFakeComm": (_I, [_P, _P, _I]),
     "SUNBW_ContextRank": (_I, [_P]),
     "SUNBW_ContextNRanks": (_I, [_P]),
+    "SUNBW_SelfTestDivision": (_I, [_P, _I64, _P, _P, _P]),
     "N_VNew_B200": (_P, [_P, _I64]),
     "N_VMake_B200": (_P, [_P, _I64, _P]),
     "N_VClone": (_P, [_P]),
@@ -206,6 +207,14 @@ class Context:
         if getattr(self, "handle", None):
             lib().SUNBW_ContextDestroy(self.handle)
             self.handle = None
+
+
+def selftest_division(ctx: "Context", a: torch.Tensor, b: torch.Tensor):
+    """(quotient mismatches, pairs checked)."""
+    out = (_I64 * 2)()
+    _check(lib().SUNBW_SelfTestDivision(ctx.handle, a.numel(), _P(a.data_ptr()), _P(b.data_ptr()), out),
+           "SUNBW_SelfTestDivision")
+    return tuple(out)
 
 
 def nccl_unique_id() -> bytes:
