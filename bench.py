@@ -319,8 +319,14 @@ def main():
                          "share": round(kms / ms_local, 4), "GB/s": round(ach, 1)}
     dom = max(kernels, key=lambda k: kernels[k]["ms_total"] if BYTES_PER_CELL.get(k) else -1)
     ach = kernels[dom]["GB/s"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if n_ax == 256 and os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(dom)        # ncu dram read+write per launch, same workload
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "kernel": dom,
+                "frac": round(ach / peak, 4), "traffic": traffic, "kernel": dom,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, this workload)",
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                 else "fallback (B200_PROFILING.md)",
                 "bytes_per_launch": BYTES_PER_CELL[dom] * G}
