@@ -380,7 +380,8 @@ BW_BrussParams bw_params(void* prob) { return ((Prob*)prob)->p; }
 bool bw_fused_advection(void* prob, const double* y, FusedAdvection* fa) {
   auto* P = (Prob*)prob;
   const BW_BrussParams& p = P->p;
-  if (p.dim != 3 || p.kind != 0 || p.reaction_only || P->nxl % 128 != 0 || p.ny < 2 || p.nz < 2)
+  if (p.dim != 3 || p.kind != 0 || p.reaction_only || P->nxl % 128 != 0 || p.ny < 2 || p.nz < 2 ||
+      P->G >= (int64_t(1) << 31))               // the kernel's tile indexing is 32-bit
     return false;
   fa->nx = P->nxl;
   fa->ny = P->nyl;
