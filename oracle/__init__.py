@@ -49,13 +49,14 @@ class SbdfParams(C.Structure):
                 ("kx", _D), ("ky", _D), ("kz", _D),
                 ("A", _D), ("B", _D), ("eps", _D),
                 ("lam_E", _D), ("lam_I", _D),
-                ("h", _D), ("rtol", _D), ("atol", _D), ("tol_nl", _D)]
+                ("h", _D), ("rtol", _D), ("atol", _D), ("tol_nl", _D),
+                ("linsol", C.c_int32), ("maxl", C.c_int32), ("lin_tol", _D)]
 
 
 class SbdfStats(C.Structure):
     _fields_ = [("steps", _I64), ("newton_iters", _I64), ("setups", _I64),
                 ("solves", _I64), ("fails", _I64), ("singular", _I64),
-                ("last_nu", _D)]
+                ("last_nu", _D), ("lin_iters", _I64)]
 
 
 def lib():
@@ -92,6 +93,8 @@ def lib():
             "oracle_bruss_ic": (None, [_I64, _I64, _I64, _D, _D, _D, _D, _D, _D, _P]),
             "oracle_sbdf_integrate": (C.c_int, [C.POINTER(SbdfParams), _P, _I64,
                                                 C.POINTER(SbdfStats), _P, _I64]),
+            "oracle_gmres": (C.c_int, [_I64, C.c_int, _P, _P, _P, _P, _P, C.c_int, _D,
+                                       C.POINTER(_D)]),
             "oracle_abi_version": (C.c_int, []),
         }
         for name, (res, args) in sig.items():
@@ -244,6 +247,23 @@ def lu_solve(LU, piv, b):
     return x
 
 
+def gmres(A, b, P=None, maxl=10, tol=1e-10):
+    """Right-preconditioned GMRES on a block-diagonal operator A (G, m, m);
+    P: None (identity) or (LU, piv) from lu_factor.  Returns (x, steps, res)."""
+    A = _f64(A); G, m, _ = A.shape
+    b = _f64(b).reshape(G * m)
+    x = np.empty_like(b)
+    res = C.c_double(0.0)
+    if P is None:
+        plu, ppiv = None, None
+    else:
+        plu = _f64(P[0]); ppiv = np.ascontiguousarray(P[1], dtype=np.int32)
+    steps = lib().oracle_gmres(G, m, _ptr(A), _ptr(plu) if plu is not None else None,
+                               _ptr(ppiv) if ppiv is not None else None, _ptr(b), _ptr(x),
+                               maxl, tol, C.byref(res))
+    return x, steps, res.value
+
+
 def block_matvec(A, x):
     A = _f64(A); G, m, _ = A.shape
     x = _f64(x).reshape(G * m)
@@ -280,13 +300,15 @@ def bruss_ic(nx, ny=1, nz=1, Lx=1.0, Ly=1.0, Lz=1.0, A=1.0, B=3.5, alpha=0.1):
 def sbdf_integrate(y0, nsteps, *, kind=0, newton_mode=0, K=3, reaction_only=False,
                    nx=1, ny=1, nz=1, kx=0.0, ky=0.0, kz=0.0,
                    A=1.0, B=3.5, eps=5e-6, lam_E=0.0, lam_I=0.0,
-                   h=1e-3, rtol=1e-6, atol=1e-9, tol_nl=1e-3, log_every=0):
+                   h=1e-3, rtol=1e-6, atol=1e-9, tol_nl=1e-3, log_every=0,
+                   linsol=0, maxl=5, lin_tol=1e-10):
     """Fixed-step IMEX SBDF1/SBDF2 with modified Newton (oracle.cpp O12/O13).
 
     Returns (rc, y, stats_dict, ylog or None)."""
     y = np.array(y0, dtype=np.float64, copy=True)
     P = SbdfParams(kind, newton_mode, K, int(bool(reaction_only)), nx, ny, nz,
-                   kx, ky, kz, A, B, eps, lam_E, lam_I, h, rtol, atol, tol_nl)
+                   kx, ky, kz, A, B, eps, lam_E, lam_I, h, rtol, atol, tol_nl,
+                   linsol, maxl, lin_tol)
     st = SbdfStats()
     ylog = None
     if log_every > 0:

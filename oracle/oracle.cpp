@@ -448,7 +448,14 @@ struct OracleSbdfParams {
   double A, B, eps;
   double lam_E, lam_I;
   double h, rtol, atol, tol_nl;
+  int32_t linsol;         // 0: block LU solve (task-local); 1: GMRES, block-LU
+                          //    preconditioner (the paper's global Newton)
+  int32_t maxl;           // GMRES Krylov dimension
+  double lin_tol;         // GMRES relative residual tolerance
 };
+
+int oracle_gmres(int64_t G, int m, const double* A, const double* PLU, const int32_t* Ppiv,
+                 const double* b, double* x, int maxl, double tol, double* res);
 
 struct OracleSbdfStats {
   int64_t steps;
@@ -458,6 +465,7 @@ struct OracleSbdfStats {
   int64_t fails;          // tolerance-mode failures (recoverable)
   int64_t singular;       // 1 + first singular block at the first failure
   double last_nu;
+  int64_t lin_iters;      // GMRES Arnoldi steps (linsol = 1)
 };
 
 static void rhs_explicit(const OracleSbdfParams* P, int64_t n, const double* y,
@@ -501,7 +509,7 @@ int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
   int64_t G = P->nx * P->ny * P->nz;
   int64_t n = 3 * G;
   std::vector<double> yprev(n), fE(n), fEprev(n), d(n), ewt(n), z(n), fI(n),
-      r(n), delta(n), M(9 * G), tmp(n);
+      r(n), delta(n), M(9 * G), Mop(9 * G), tmp(n);
   std::vector<int32_t> piv(3 * G);
   std::memset(st, 0, sizeof(*st));
   int64_t nlog = 0;
@@ -528,6 +536,7 @@ int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
     std::memcpy(z.data(), y, n * sizeof(double));
     jac_implicit(P, G, z.data(), M.data());
     oracle_scale_add_identity(G, 3, -gamma, M.data());
+    if (P->linsol == 1) Mop = M;            // the operator; M becomes its LU
     int64_t sing = oracle_lu_factor(G, 3, M.data(), piv.data());
     st->setups++;
     if (sing) { st->singular = sing; st->fails++; return 1; }
@@ -538,7 +547,13 @@ int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
       double c3[3] = {1.0, gamma, -1.0};
       const double* X3[3] = {d.data(), fI.data(), z.data()};
       oracle_linear_combination(3, c3, X3, n, r.data());
-      oracle_lu_solve(G, 3, M.data(), piv.data(), r.data(), delta.data());
+      if (P->linsol == 1) {
+        double res = 0.0;
+        st->lin_iters += oracle_gmres(G, 3, Mop.data(), M.data(), piv.data(), r.data(),
+                                      delta.data(), P->maxl, P->lin_tol, &res);
+      } else {
+        oracle_lu_solve(G, 3, M.data(), piv.data(), r.data(), delta.data());
+      }
       st->solves++;
       oracle_linear_sum(n, 1.0, z.data(), 1.0, delta.data(), z.data());
       double nu = oracle_wrms(n, delta.data(), ewt.data());
@@ -562,6 +577,91 @@ int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
     }
   }
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// GMRES (the SPGMR Krylov solver of P:299 §5, used by the paper's "global"
+// Newton configuration with the block solve as preconditioner, §7).
+// Right-preconditioned GMRES(maxl) without restarts, x0 = 0:
+//   β = ‖b‖₂, V₀ = b/β
+//   for j = 0..maxl-1:
+//     w = A P⁻¹ V_j
+//     h_ij = w·V_i (i ≤ j)                  — classical Gram–Schmidt: all
+//     w = w − Σ_i h_ij V_i                    inner products from the same w
+//     h_{j+1,j} = ‖w‖₂, V_{j+1} = w / h_{j+1,j}
+//     Givens rotations on column j; |g_{j+1}| = residual norm
+//     stop if |g_{j+1}| ≤ tol·β (or h_{j+1,j} == 0)
+//   y = H⁻¹ g (back substitution), x = P⁻¹ Σ_i y_i V_i
+// A: G blocks of m×m (row-major), PLU/Ppiv: LU factors + pivots of the
+// block preconditioner (oracle_lu_factor format), or NULL for P = I.
+// Returns the number of Arnoldi steps; *res = final |g_{j+1}|.
+static void block_solve_or_copy(int64_t G, int m, const double* LU, const int32_t* piv,
+                                const double* v, double* out) {
+  if (LU)
+    oracle_lu_solve(G, m, LU, piv, v, out);
+  else
+    std::memcpy(out, v, sizeof(double) * G * m);
+}
+
+int oracle_gmres(int64_t G, int m, const double* A, const double* PLU, const int32_t* Ppiv,
+                 const double* b, double* x, int maxl, double tol, double* res) {
+  const int64_t n = G * m;
+  std::vector<std::vector<double>> V(maxl + 1, std::vector<double>(n));
+  std::vector<double> H((maxl + 1) * maxl, 0.0), g(maxl + 1, 0.0), cs(maxl), sn(maxl);
+  std::vector<double> z(n), w(n);
+  double beta = std::sqrt(oracle_dot(n, b, b));
+  if (beta == 0.0) {
+    for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
+    *res = 0.0;
+    return 0;
+  }
+  oracle_scale(n, 1.0 / beta, b, V[0].data());
+  g[0] = beta;
+  int j = 0, steps = 0;
+  for (; j < maxl; ++j) {
+    block_solve_or_copy(G, m, PLU, Ppiv, V[j].data(), z.data());
+    oracle_block_matvec(G, m, A, z.data(), w.data());
+    for (int i = 0; i <= j; ++i) H[i * maxl + j] = oracle_dot(n, w.data(), V[i].data());
+    for (int i = 0; i <= j; ++i) {
+      double c = -H[i * maxl + j];
+      for (int64_t k = 0; k < n; ++k) {
+        double t = c * V[i][k];
+        w[k] = w[k] + t;
+      }
+    }
+    double hn = std::sqrt(oracle_dot(n, w.data(), w.data()));
+    H[(j + 1) * maxl + j] = hn;
+    if (hn != 0.0) oracle_scale(n, 1.0 / hn, w.data(), V[j + 1].data());
+    for (int i = 0; i < j; ++i) {            // previous rotations on column j
+      double a = H[i * maxl + j], c = H[(i + 1) * maxl + j];
+      H[i * maxl + j] = cs[i] * a + sn[i] * c;
+      H[(i + 1) * maxl + j] = -sn[i] * a + cs[i] * c;
+    }
+    double a = H[j * maxl + j], c = H[(j + 1) * maxl + j];
+    double r = std::hypot(a, c);
+    cs[j] = a / r;
+    sn[j] = c / r;
+    H[j * maxl + j] = r;
+    H[(j + 1) * maxl + j] = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    steps = j + 1;
+    if (std::fabs(g[j + 1]) <= tol * beta || hn == 0.0) break;
+  }
+  std::vector<double> y(steps);
+  for (int i = steps - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int k = i + 1; k < steps; ++k) s -= H[i * maxl + k] * y[k];
+    y[i] = s / H[i * maxl + i];
+  }
+  for (int64_t k = 0; k < n; ++k) {
+    double s = 0.0;
+    for (int i = 0; i < steps; ++i) s += y[i] * V[i][k];
+    w[k] = s;
+  }
+  block_solve_or_copy(G, m, PLU, Ppiv, w.data(), x);
+  *res = std::fabs(g[steps]);
+  return steps;
 }
 
 int oracle_abi_version(void) { return 1; }

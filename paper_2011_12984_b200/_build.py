@@ -14,7 +14,8 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libsunbw.so")
 
-SOURCES = ["context.cu", "nvector.cu", "blockdiag.cu", "brusselator.cu", "stepper.cu", "fused.cu"]
+SOURCES = ["context.cu", "nvector.cu", "blockdiag.cu", "brusselator.cu", "stepper.cu", "fused.cu",
+           "gmres.cu"]
 HEADERS = ["sunbw_internal.h", "sunbw_device.cuh", "pipeline.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

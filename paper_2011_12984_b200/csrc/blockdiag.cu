@@ -515,6 +515,7 @@ extern "C" SUNLinearSolver SUNLinSol_B200BatchedLU(N_Vector y, SUNMatrix A) {
 }
 
 extern "C" int SUNLinSolSetup(SUNLinearSolver S0, SUNMatrix A) {
+  if (S0 && S0->type == 1) return sunbw::spgmr_setup(S0, A);
   auto* S = (LinSolImpl*)S0;
   if (!S || !A) return SUNBW_ERR_ARG;
   if (A->ctx != S->ctx) return ctx_set_err(S->ctx, SUNBW_ERR_CONTEXT);
@@ -528,7 +529,8 @@ extern "C" int SUNLinSolSetup(SUNLinearSolver S0, SUNMatrix A) {
   return f > 0 ? SUNBW_RECOV_SINGULAR : 0;
 }
 
-extern "C" int SUNLinSolSolve(SUNLinearSolver S, SUNMatrix A, N_Vector x, N_Vector b, double) {
+extern "C" int SUNLinSolSolve(SUNLinearSolver S, SUNMatrix A, N_Vector x, N_Vector b, double tol) {
+  if (S && S->type == 1) return sunbw::spgmr_solve(S, A, x, b, tol);
   if (!S || !A || !x || !b) return SUNBW_ERR_ARG;
   if (x->ctx != S->ctx || b->ctx != S->ctx || A->ctx != S->ctx) return ctx_set_err(S->ctx, SUNBW_ERR_CONTEXT);
   if (x->local_len != S->nblocks * S->m || b->local_len != x->local_len)
@@ -537,6 +539,7 @@ extern "C" int SUNLinSolSolve(SUNLinearSolver S, SUNMatrix A, N_Vector x, N_Vect
 }
 
 extern "C" int64_t SUNLinSolLastFlag(SUNLinearSolver S0) {
+  if (S0 && S0->type == 1) return S0->last_flag;
   auto* S = (LinSolImpl*)S0;
   if (!S) return SUNBW_ERR_ARG;
   if (S->flag_pending) {
@@ -559,6 +562,7 @@ extern "C" int SUNLinSol_B200BatchedLU_SetDeferredCheck(SUNLinearSolver S, int d
 extern "C" int32_t* SUNLinSol_B200BatchedLU_Pivots(SUNLinearSolver S) { return S ? S->d_piv : nullptr; }
 
 extern "C" void SUNLinSolFree(SUNLinearSolver S0) {
+  if (S0 && S0->type == 1) return sunbw::spgmr_free(S0);
   auto* S = (LinSolImpl*)S0;
   if (!S) return;
   if (S->d_piv) cudaFree(S->d_piv);

@@ -38,8 +38,6 @@ int bw_jacobian(void* prob, const double* y, double* J);
 int bw_halo(void* prob, const double* y);
 int bw_advection_stencil(void* prob, const double* y, double* f);
 int64_t bw_local_cells(void* prob);
-int lu_factor_noreset(SUNBW_Context, int64_t G, int m, double* A, int32_t* piv,
-                      unsigned long long* d_first);
 int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, double h,
                  double rtol, double atol, const double* y, const double* yp, const double* fE,
                  const double* fEp, double* z, double* partials, unsigned long long* d_first,
@@ -66,6 +64,7 @@ struct Stepper {
   double* d_scal;        // [0] ewt min, [1..K] nu per iteration
   int* d_err;            // 1: non-positive ewt denominator seen
   double* d_partials;    // fused mode per-CTA partials
+  SUNLinearSolver gm = nullptr;   // linsol 1: SPGMR, block-LU preconditioner
   int64_t step = 0;
   double t = 0.0;
   BW_StepperStats st{};
@@ -191,7 +190,13 @@ int enqueue_step(Stepper* S, bool first) {
   { Timed t(S, BW_K_PREDICT); TRY(sunbw::scale(ctx, n, 1.0, y, z, nullptr)); }
   { Timed t(S, BW_K_JACOBIAN); TRY(sunbw::bw_jacobian(S->prob, z, S->M)); }
   { Timed t(S, BW_K_SCALEADDI); TRY(sunbw::scale_add_identity(ctx, G, 3, -gamma, S->M)); }
-  { Timed t(S, BW_K_LU_SETUP); TRY(sunbw::lu_factor_noreset(ctx, G, 3, S->M, S->piv, S->d_first)); }
+  {
+    Timed t(S, BW_K_LU_SETUP);
+    if (S->gm)   // global Newton: M stays the GMRES operator, its LU preconditions
+      TRY(sunbw::spgmr_setup_raw(S->gm, S->M, S->d_first));
+    else
+      TRY(sunbw::lu_factor_noreset(ctx, G, 3, S->M, S->piv, S->d_first));
+  }
 
   const bool tol = o.newton_mode == 1;
   if (tol) {
@@ -213,7 +218,16 @@ int enqueue_step(Stepper* S, bool first) {
       const double* X3[3] = {S->d, S->fI, z};
       TRY(sunbw::linear_combination(ctx, n, 3, c3, X3, S->r, nullptr));
     }
-    { Timed t(S, BW_K_LU_SOLVE); TRY(sunbw::lu_solve(ctx, G, 3, S->M, S->piv, S->r, S->delta)); }
+    {
+      Timed t(S, BW_K_LU_SOLVE);
+      if (S->gm) {
+        int steps = sunbw::spgmr_solve_raw(S->gm, S->M, S->delta, S->r, o.lin_tol);
+        TRY(steps);
+        S->st.lin_iters += steps;
+      } else {
+        TRY(sunbw::lu_solve(ctx, G, 3, S->M, S->piv, S->r, S->delta));
+      }
+    }
     { Timed t(S, BW_K_UPDATE); TRY(sunbw::linear_sum(ctx, n, 1.0, z, 1.0, S->delta, z, nullptr)); }
     {
       Timed t(S, BW_K_WRMS);
@@ -284,7 +298,8 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   *out = nullptr;
   if (opt->K < 1 || opt->K > kMaxK || !(opt->h > 0) || (opt->newton_mode != 0 && opt->newton_mode != 1))
     return SUNBW_ERR_ARG;
-  if (opt->fused && (opt->newton_mode != 0 || opt->K > 8)) return SUNBW_ERR_UNSUPPORTED;
+  if (opt->fused && (opt->newton_mode != 0 || opt->K > 8 || opt->linsol != 0)) return SUNBW_ERR_UNSUPPORTED;
+  if (opt->linsol != 0 && (opt->linsol != 1 || opt->maxl < 1 || opt->maxl > 60)) return SUNBW_ERR_ARG;
   SUNBW_Context ctx = y0->ctx;
   int64_t G = sunbw::bw_local_cells(prob);
   if (y0->local_len != 3 * G) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
@@ -293,7 +308,7 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   S->ctx = ctx;
   S->opt = *opt;
   if (S->opt.timing || (ctx->comm && !ctx->comm->capturable())) S->opt.use_graph = 0;
-  if (S->opt.newton_mode == 1) S->opt.use_graph = 0;
+  if (S->opt.newton_mode == 1 || S->opt.linsol == 1) S->opt.use_graph = 0;   // host decisions
   S->G = G;
   S->n = 3 * G;
   S->nglobal = y0->global_len;
@@ -310,6 +325,10 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
     if (!e) e = alloc(S, &S->delta, n);
     if (!e) e = alloc(S, &S->M, 9 * G);
     if (!e && cudaMalloc(&S->piv, sizeof(int32_t) * (G > 0 ? G : 1)) != cudaSuccess) e = SUNBW_ERR_MEM;
+  }
+  if (!e && opt->linsol == 1) {
+    S->gm = sunbw::spgmr_create(ctx, G, 3, opt->maxl, true);
+    if (!S->gm) e = SUNBW_ERR_MEM;
   }
   if (!e) e = alloc(S, &S->d_scal, kMaxK + 8);
   if (!e) e = alloc(S, &S->d_partials, (int64_t)(ctx->nsm * 16) * (kMaxK + 1));
@@ -429,6 +448,7 @@ extern "C" int BW_StepperDestroy(void* stepper) {
   if (S->piv) cudaFree(S->piv);
   if (S->d_first) cudaFree(S->d_first);
   if (S->d_err) cudaFree(S->d_err);
+  if (S->gm) sunbw::spgmr_free(S->gm);
   delete S;
   return 0;
 }

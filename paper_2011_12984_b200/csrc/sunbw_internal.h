@@ -77,6 +77,7 @@ struct _SUNMatrix {
 };
 
 struct _SUNLinearSolver {
+  int type = 0;                 // 0: batched block LU, 1: SPGMR (gmres.cu)
   SUNBW_Context ctx;
   int64_t nblocks;
   int m;
@@ -132,6 +133,20 @@ int lu_solve(SUNBW_Context, int64_t G, int m, const double* LU,
              const int32_t* piv, const double* b, double* x);
 int block_matvec(SUNBW_Context, int64_t G, int m, const double* A,
                  const double* x, double* y);
+
+int lu_factor_noreset(SUNBW_Context, int64_t G, int m, double* A, int32_t* piv,
+                      unsigned long long* d_first);
+
+// SPGMR (gmres.cu): dispatched from the SUNLinSol* entry points
+SUNLinearSolver spgmr_create(SUNBW_Context ctx, int64_t G, int m, int maxl, bool block_prec);
+int spgmr_setup_raw(SUNLinearSolver S, const double* A, unsigned long long* d_first_accum);
+int spgmr_setup(SUNLinearSolver S, SUNMatrix A);
+int spgmr_solve(SUNLinearSolver S, SUNMatrix A, N_Vector x, N_Vector b, double tol);
+void spgmr_free(SUNLinearSolver S);
+// device-pointer form used by the driver: operator A (G blocks of 3x3),
+// solves A x = b to relative residual tol; returns Arnoldi steps or < 0
+int spgmr_solve_raw(SUNLinearSolver S, const double* A, double* x, const double* b, double tol);
+int64_t spgmr_last_iters(SUNLinearSolver S);
 
 // geometry for the fused step kernel's in-kernel 3D advection
 struct FusedAdvection {

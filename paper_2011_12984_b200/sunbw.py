@@ -44,12 +44,14 @@ class BW_BrussParams(C.Structure):
 class BW_StepperOptions(C.Structure):
     _fields_ = [("h", _D), ("newton_mode", C.c_int32), ("K", C.c_int32), ("tol_nl", _D),
                 ("rtol", _D), ("atol", _D), ("use_graph", C.c_int32), ("timing", C.c_int32),
-                ("fused", C.c_int32), ("fused_advection", C.c_int32)]
+                ("fused", C.c_int32), ("fused_advection", C.c_int32),
+                ("linsol", C.c_int32), ("maxl", C.c_int32), ("lin_tol", _D)]
 
 
 class BW_StepperStats(C.Structure):
     _fields_ = [("steps", _I64), ("newton_iters", _I64), ("setups", _I64), ("solves", _I64),
-                ("fails", _I64), ("singular", _I64), ("last_nu", _D), ("t", _D)]
+                ("fails", _I64), ("singular", _I64), ("last_nu", _D), ("t", _D),
+                ("lin_iters", _I64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -113,6 +115,9 @@ _SIGS = {
     "SUNLinSol_B200BatchedLU_SetDeferredCheck": (_I, [_P, _I]),
     "SUNLinSol_B200BatchedLU_Pivots": (_P, [_P]),
     "SUNLinSolFree": (None, [_P]),
+    "SUNLinSol_B200SPGMR": (_P, [_P, _P, _I, _I]),
+    "SUNLinSolNumIters": (_I64, [_P]),
+    "SUNLinSolResNorm": (_D, [_P]),
     "BW_ProblemCreate": (_I, [_P, C.POINTER(BW_BrussParams), C.POINTER(_P)]),
     "BW_ProblemDestroy": (_I, [_P]),
     "BW_ProblemLocalCells": (_I64, [_P]),
@@ -351,10 +356,16 @@ def SUNMatMatvec(A: SUNMatrix, x: NVector, y: NVector) -> int:
 
 
 class SUNLinearSolver:
-    def __init__(self, y: NVector, A: SUNMatrix):
-        h = lib().SUNLinSol_B200BatchedLU(y, A)
+    """Batched block LU (default) or, with spgmr_maxl, SPGMR (GMRES with the
+    block LU as optional preconditioner)."""
+
+    def __init__(self, y: NVector, A: SUNMatrix, spgmr_maxl: int = 0, block_prec: bool = True):
+        if spgmr_maxl:
+            h = lib().SUNLinSol_B200SPGMR(y, A, spgmr_maxl, int(block_prec))
+        else:
+            h = lib().SUNLinSol_B200BatchedLU(y, A)
         if not h:
-            raise SunbwError("SUNLinSol_B200BatchedLU failed")
+            raise SunbwError("SUNLinearSolver construction failed")
         self.handle = h
         self.nblocks = A.t.shape[0]
 
@@ -398,6 +409,14 @@ def SUNLinSolSetup(S: SUNLinearSolver, A: SUNMatrix) -> int:
 
 def SUNLinSolSolve(S: SUNLinearSolver, A: SUNMatrix, x: NVector, b: NVector, tol=0.0) -> int:
     return _check(lib().SUNLinSolSolve(S, A, x, b, tol), "SUNLinSolSolve")
+
+
+def SUNLinSolNumIters(S: SUNLinearSolver) -> int:
+    return lib().SUNLinSolNumIters(S)
+
+
+def SUNLinSolResNorm(S: SUNLinearSolver) -> float:
+    return lib().SUNLinSolResNorm(S)
 
 
 def SUNLinSolLastFlag(S: SUNLinearSolver) -> int:
@@ -463,9 +482,9 @@ def BW_ReactionJacobian(P: Problem, y: NVector, J: SUNMatrix) -> int:
 
 def stepper_options(h=1e-3, newton_mode=0, K=3, tol_nl=1e-3, rtol=1e-6, atol=1e-9,
                     use_graph=True, timing=False, fused=False,
-                    fused_advection=True) -> BW_StepperOptions:
+                    fused_advection=True, linsol=0, maxl=5, lin_tol=1e-10) -> BW_StepperOptions:
     return BW_StepperOptions(h, newton_mode, K, tol_nl, rtol, atol, int(use_graph), int(timing),
-                             int(fused), int(fused_advection))
+                             int(fused), int(fused_advection), linsol, maxl, lin_tol)
 
 
 class Stepper:
