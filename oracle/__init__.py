@@ -59,6 +59,16 @@ class SbdfStats(C.Structure):
                 ("last_nu", _D), ("lin_iters", _I64)]
 
 
+class ArkParams(C.Structure):
+    _fields_ = [("prob", SbdfParams), ("h0", _D), ("t_end", _D), ("maxnl", C.c_int32),
+                ("max_steps", C.c_int32), ("fixed", C.c_int32), ("pad_", C.c_int32)]
+
+
+class ArkStats(C.Structure):
+    _fields_ = [("accepted", _I64), ("rejected_err", _I64), ("rejected_nl", _I64),
+                ("newton_iters", _I64), ("setups", _I64), ("t", _D), ("h_last", _D)]
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -95,6 +105,8 @@ def lib():
                                                 C.POINTER(SbdfStats), _P, _I64]),
             "oracle_gmres": (C.c_int, [_I64, C.c_int, _P, _P, _P, _P, _P, C.c_int, _D,
                                        C.POINTER(_D)]),
+            "oracle_ark_tableau": (None, [_P, _P, _P, _P, _P]),
+            "oracle_ark_integrate": (C.c_int, [C.POINTER(ArkParams), _P, C.POINTER(ArkStats)]),
             "oracle_abi_version": (C.c_int, []),
         }
         for name, (res, args) in sig.items():
@@ -318,3 +330,25 @@ def sbdf_integrate(y0, nsteps, *, kind=0, newton_mode=0, K=3, reaction_only=Fals
                                      log_every)
     stats = {k: getattr(st, k) for k, _ in SbdfStats._fields_}
     return rc, y, stats, ylog
+
+
+# ------------------------------------------------------- adaptive IMEX ARK
+def ark_tableau():
+    """(AE 4x4, AI 4x4, b, d, c) of ARK3(2)4L[2]SA as doubles."""
+    AE, AI = np.zeros((4, 4)), np.zeros((4, 4))
+    b, d, c = np.zeros(4), np.zeros(4), np.zeros(4)
+    lib().oracle_ark_tableau(_ptr(AE), _ptr(AI), _ptr(b), _ptr(d), _ptr(c))
+    return AE, AI, b, d, c
+
+
+def ark_integrate(y0, t_end, *, h0=1e-4, maxnl=3, max_steps=100000, fixed=False, kind=0,
+                  reaction_only=False, nx=1, ny=1, nz=1, kx=0.0, ky=0.0, kz=0.0, A=1.0, B=3.5,
+                  eps=5e-6, lam_E=0.0, lam_I=0.0, rtol=1e-6, atol=1e-9, tol_nl=0.1):
+    """Adaptive IMEX ARK3(2)4L[2]SA (oracle.cpp).  Returns (rc, y, stats)."""
+    y = np.array(y0, dtype=np.float64, copy=True)
+    P = SbdfParams(kind, 1, maxnl, int(bool(reaction_only)), nx, ny, nz, kx, ky, kz, A, B, eps,
+                   lam_E, lam_I, h0, rtol, atol, tol_nl, 0, 1, 0.0)
+    AP = ArkParams(P, h0, t_end, maxnl, max_steps, int(bool(fixed)), 0)
+    st = ArkStats()
+    rc = lib().oracle_ark_integrate(C.byref(AP), _ptr(y), C.byref(st))
+    return rc, y, {k: getattr(st, k) for k, _ in ArkStats._fields_}

@@ -664,6 +664,173 @@ int oracle_gmres(int64_t G, int m, const double* A, const double* PLU, const int
   return steps;
 }
 
+// ---------------------------------------------------------------------------
+// Adaptive IMEX additive Runge–Kutta — the paper's integrator (ARKODE IMEX,
+// advection explicit, reaction implicit; temporal error control
+// through global reductions and step recomputation with a smaller h when a
+// nonlinear solve fails).  Tableau: ARK3(2)4L[2]SA of Kennedy and
+// Carpenter (the paper names no tableau; SPEC S:418 picks this one; DESIGN
+// R26).  Stages i = 1..4 (a^I_11 = 0: the first stage is explicit):
+//   Z_i = y_n + h Σ_{j<i} (aE_ij FE_j + aI_ij FI_j) + h γ f_I(Z_i)
+//   FE_i = f_E(Z_i), FI_i = f_I(Z_i)
+//   y_{n+1} = y_n + h Σ_i b_i (FE_i + FI_i)
+//   e = h Σ_i (b_i − d_i)(FE_i + FI_i),  dsm = WRMS(e, ewt(y_n))
+// Stage solve: modified Newton, M = I − hγ J(Z_{i−1}) (predictor: previous
+// stage), r = rhs + hγ f_I(Z) − Z, δ = M⁻¹r, Z += δ, ν = WRMS(δ, ewt);
+// converged when ν ≤ tol_nl, failure after maxnl iterations → the step is
+// recomputed with h·0.25.  Step control (I-controller, DESIGN R26):
+// accept if dsm ≤ 1; h ← h·min(5, max(0.2, 0.9·dsm^(−1/3))) (rejection: max
+// factor 1).  The Newton matrix of a stage is the Jacobian of the reaction
+// only, exactly block diagonal.
+// ---------------------------------------------------------------------------
+
+struct OracleArkParams {
+  OracleSbdfParams prob;  // kind, grid, kappas, A/B/eps, lambdas, rtol/atol, tol_nl
+  double h0;              // initial step
+  double t_end;           // integrate [0, t_end]
+  int32_t maxnl;          // Newton iterations per stage
+  int32_t max_steps;      // attempts (accepted + rejected) limit
+  int32_t fixed;          // 1: constant h, every step accepted (order pins)
+  int32_t pad_;
+};
+
+struct OracleArkStats {
+  int64_t accepted, rejected_err, rejected_nl, newton_iters, setups;
+  double t, h_last;
+};
+
+static const double ARK_G = 1767732205903.0 / 4055673282236.0;
+static const double ARK_C[4] = {0.0, 1767732205903.0 / 2027836641118.0, 3.0 / 5.0, 1.0};
+static const double ARK_AE[4][4] = {
+    {0, 0, 0, 0},
+    {1767732205903.0 / 2027836641118.0, 0, 0, 0},
+    {5535828885825.0 / 10492691773637.0, 788022342437.0 / 10882634858940.0, 0, 0},
+    {6485989280629.0 / 16251701735622.0, -4246266847089.0 / 9704473918619.0,
+     10755448449292.0 / 10357097424841.0, 0}};
+static const double ARK_AI[4][4] = {
+    {0, 0, 0, 0},
+    {1767732205903.0 / 4055673282236.0, 1767732205903.0 / 4055673282236.0, 0, 0},
+    {2746238789719.0 / 10658868560708.0, -640167445237.0 / 6845629431997.0,
+     1767732205903.0 / 4055673282236.0, 0},
+    {1471266399579.0 / 7840856788654.0, -4482444167858.0 / 7529755066697.0,
+     11266239266428.0 / 11593286722821.0, 1767732205903.0 / 4055673282236.0}};
+static const double ARK_B[4] = {1471266399579.0 / 7840856788654.0, -4482444167858.0 / 7529755066697.0,
+                                11266239266428.0 / 11593286722821.0, 1767732205903.0 / 4055673282236.0};
+static const double ARK_D[4] = {2756255671327.0 / 12835298489170.0, -10771552573575.0 / 22201958757719.0,
+                                9247589265047.0 / 10645013368117.0, 2193209047091.0 / 5459859503100.0};
+
+// the tableau as doubles (for the order-condition pins)
+void oracle_ark_tableau(double* AE16, double* AI16, double* b4, double* d4, double* c4) {
+  for (int i = 0; i < 4; ++i) {
+    b4[i] = ARK_B[i];
+    d4[i] = ARK_D[i];
+    c4[i] = ARK_C[i];
+    for (int j = 0; j < 4; ++j) {
+      AE16[4 * i + j] = ARK_AE[i][j];
+      AI16[4 * i + j] = ARK_AI[i][j];
+    }
+  }
+}
+
+// Returns 0 (reached t_end), 1 (max_steps exhausted) or 2 (h underflow).
+int oracle_ark_integrate(const OracleArkParams* AP, double* y, OracleArkStats* st) {
+  const OracleSbdfParams* P = &AP->prob;
+  int64_t G = P->nx * P->ny * P->nz;
+  int64_t n = 3 * G;
+  std::vector<double> ewt(n), tmp(n), rhs(n), Z(n), r(n), delta(n), ynew(n), err(n), fI(n),
+      M(9 * G);
+  std::vector<int32_t> piv(3 * G);
+  std::vector<std::vector<double>> FE(4, std::vector<double>(n)), FI(4, std::vector<double>(n));
+  std::memset(st, 0, sizeof(*st));
+  double t = 0.0, h = AP->h0;
+  int attempts = 0;
+  // done when the remaining interval is below 1e-12·max(1, |t_end|)
+  // (accumulated rounding of t; DESIGN R26)
+  while (AP->t_end - t > 1e-12 * std::fmax(1.0, std::fabs(AP->t_end))) {
+    if (attempts++ >= AP->max_steps) { st->t = t; st->h_last = h; return 1; }
+    if (t + h > AP->t_end) h = AP->t_end - t;
+    if (h < 1e-14 * (1.0 + t)) { st->t = t; st->h_last = h; return 2; }
+    // ewt from y_n
+    oracle_abs(n, y, tmp.data());
+    oracle_scale(n, P->rtol, tmp.data(), tmp.data());
+    oracle_add_const(n, tmp.data(), P->atol, tmp.data());
+    oracle_inv(n, tmp.data(), ewt.data());
+    const double hg = h * ARK_G;
+    bool nl_fail = false;
+    for (int i = 0; i < 4 && !nl_fail; ++i) {
+      if (i == 0) {
+        std::memcpy(Z.data(), y, n * sizeof(double));
+      } else {
+        // rhs = y_n + h Σ_{j<i} (aE_ij FE_j + aI_ij FI_j)
+        std::vector<double> c;
+        std::vector<const double*> X;
+        c.push_back(1.0);
+        X.push_back(y);
+        for (int j = 0; j < i; ++j) {
+          c.push_back(h * ARK_AE[i][j]); X.push_back(FE[j].data());
+          c.push_back(h * ARK_AI[i][j]); X.push_back(FI[j].data());
+        }
+        oracle_linear_combination((int)c.size(), c.data(), X.data(), n, rhs.data());
+        // modified Newton from the previous stage value (Z holds Z_{i-1})
+        jac_implicit(P, G, Z.data(), M.data());
+        oracle_scale_add_identity(G, 3, -hg, M.data());
+        st->setups++;
+        if (oracle_lu_factor(G, 3, M.data(), piv.data())) { nl_fail = true; break; }
+        bool conv = false;
+        for (int it = 0; it < AP->maxnl; ++it) {
+          rhs_implicit(P, G, Z.data(), fI.data());
+          double c3[3] = {1.0, hg, -1.0};
+          const double* X3[3] = {rhs.data(), fI.data(), Z.data()};
+          oracle_linear_combination(3, c3, X3, n, r.data());
+          oracle_lu_solve(G, 3, M.data(), piv.data(), r.data(), delta.data());
+          oracle_linear_sum(n, 1.0, Z.data(), 1.0, delta.data(), Z.data());
+          st->newton_iters++;
+          if (oracle_wrms(n, delta.data(), ewt.data()) <= P->tol_nl) { conv = true; break; }
+        }
+        if (!conv) { nl_fail = true; break; }
+      }
+      rhs_explicit(P, n, Z.data(), FE[i].data());
+      rhs_implicit(P, G, Z.data(), FI[i].data());
+    }
+    if (nl_fail) {               // recompute the step with a smaller h
+      st->rejected_nl++;
+      h *= 0.25;
+      continue;
+    }
+    // y_{n+1} and the embedded error
+    {
+      std::vector<double> c, ce;
+      std::vector<const double*> X, Xe;
+      c.push_back(1.0);
+      X.push_back(y);
+      for (int i = 0; i < 4; ++i) {
+        c.push_back(h * ARK_B[i]); X.push_back(FE[i].data());
+        c.push_back(h * ARK_B[i]); X.push_back(FI[i].data());
+        double be = h * (ARK_B[i] - ARK_D[i]);
+        ce.push_back(be); Xe.push_back(FE[i].data());
+        ce.push_back(be); Xe.push_back(FI[i].data());
+      }
+      oracle_linear_combination((int)c.size(), c.data(), X.data(), n, ynew.data());
+      oracle_linear_combination((int)ce.size(), ce.data(), Xe.data(), n, err.data());
+    }
+    double dsm = oracle_wrms(n, err.data(), ewt.data());
+    double fac = dsm > 0.0 ? 0.9 * std::pow(dsm, -1.0 / 3.0) : 5.0;
+    if (AP->fixed) { dsm = 0.0; fac = 1.0; }
+    if (dsm <= 1.0) {
+      std::memcpy(y, ynew.data(), n * sizeof(double));
+      t += h;
+      st->accepted++;
+      h *= std::fmin(5.0, std::fmax(0.2, fac));
+    } else {
+      st->rejected_err++;
+      h *= std::fmin(1.0, std::fmax(0.2, fac));
+    }
+  }
+  st->t = t;
+  st->h_last = h;
+  return 0;
+}
+
 int oracle_abi_version(void) { return 1; }
 
 }  // extern "C"

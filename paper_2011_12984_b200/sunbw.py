@@ -57,6 +57,19 @@ class BW_StepperStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class BW_ArkOptions(C.Structure):
+    _fields_ = [("h0", _D), ("rtol", _D), ("atol", _D), ("tol_nl", _D), ("maxnl", C.c_int32),
+                ("max_steps", C.c_int32), ("fixed", C.c_int32), ("pad_", C.c_int32)]
+
+
+class BW_ArkStats(C.Structure):
+    _fields_ = [("accepted", _I64), ("rejected_err", _I64), ("rejected_nl", _I64),
+                ("newton_iters", _I64), ("setups", _I64), ("t", _D), ("h_last", _D)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _SIGS = {
     "SUNBW_ContextCreate": (_I, [_I, _P, C.POINTER(_P)]),
     "SUNBW_ContextSetStream": (_I, [_P, _P]),
@@ -131,6 +144,9 @@ _SIGS = {
     "BW_StepperReset": (_I, [_P, _P, _D]),
     "BW_StepperKernelTimes": (_I, [_P, _P, _P, _I]),
     "BW_StepperDestroy": (_I, [_P]),
+    "BW_ArkCreate": (_I, [_P, _P, C.POINTER(BW_ArkOptions), C.POINTER(_P)]),
+    "BW_ArkEvolve": (_I, [_P, _D, _P, C.POINTER(BW_ArkStats)]),
+    "BW_ArkDestroy": (_I, [_P]),
 }
 
 
@@ -517,4 +533,26 @@ class Stepper:
     def destroy(self):
         if self.handle:
             lib().BW_StepperDestroy(self.handle)
+            self.handle = None
+
+
+class Ark:
+    """Adaptive IMEX ARK3(2)4L[2]SA integrator (BW_ArkCreate / BW_ArkEvolve)."""
+
+    def __init__(self, P: Problem, y0: NVector, h0=1e-4, rtol=1e-6, atol=1e-9, tol_nl=0.1, maxnl=3,
+                 max_steps=100000, fixed=False):
+        self.opts = BW_ArkOptions(h0, rtol, atol, tol_nl, maxnl, max_steps, int(bool(fixed)), 0)
+        h = _P()
+        _check(lib().BW_ArkCreate(P, y0, C.byref(self.opts), C.byref(h)), "BW_ArkCreate")
+        self.handle = h.value
+
+    def evolve(self, t_end: float, y_out: NVector | None = None):
+        st = BW_ArkStats()
+        rc = lib().BW_ArkEvolve(self.handle, t_end, y_out if y_out is not None else None, C.byref(st))
+        _check(rc, "BW_ArkEvolve")
+        return rc, st.as_dict()
+
+    def destroy(self):
+        if self.handle:
+            lib().BW_ArkDestroy(self.handle)
             self.handle = None
