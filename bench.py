@@ -231,6 +231,84 @@ def nvector_ops(S, ctx, torch, peak, n=100_000_000, reps=20):
     return out
 
 
+def other_configs(S, ctx, torch):
+    """The other BASELINE.json configs, measured briefly on this GPU (fixed
+    K = 3, h = 1e-3, device-timed with CUDA events):
+      C1: 1D Brusselator, 64 cells, t in [0, 1] (1000 steps) — launch-bound:
+          composed step replayed from CUDA graphs, and the fused kernel;
+      C3: 3D, 128^3 cells, fused single-kernel step (graph replay);
+      C4: 1e7 independent reaction cells (batched block Newton only): fused
+          steps, and one composed Newton iteration (f_I, residual LC, block
+          solve, update, WRMS) with its algorithmic bytes (388 B/cell)."""
+    out = {}
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    def stepper_rate(params, G, steps, **opt):
+        P = S.Problem(ctx, params)
+        y0 = torch.empty(3 * G, dtype=torch.float64, device="cuda")
+        vy = S.NVector(ctx, y0)
+        S.BW_InitialCondition(P, vy)
+        st = S.Stepper(P, vy, S.stepper_options(h=1e-3, K=3, **opt))
+        st.advance(5)                                   # warm-up, graph capture
+        ms = timed(lambda: st.advance(steps))
+        st.destroy(); P.destroy()
+        return steps / (ms * 1e-3)
+
+    c1 = S.bruss_params(dim=1, nx=64)
+    out["C1_1D_64cells"] = {
+        "composed_graph_steps_per_s": round(stepper_rate(c1, 64, 1000, use_graph=True), 1),
+        "fused_graph_steps_per_s": round(stepper_rate(c1, 64, 1000, use_graph=True, fused=True), 1)}
+    c3 = S.bruss_params(dim=3, nx=128, ny=128, nz=128)
+    r3 = stepper_rate(c3, 128 ** 3, 200, use_graph=True, fused=True)
+    out["C3_3D_128cubed"] = {"fused_steps_per_s": round(r3, 1), "cell_steps_per_s": r3 * 128 ** 3}
+    G4 = 10_000_000
+    c4 = S.bruss_params(dim=1, nx=G4, reaction_only=True)
+    r4 = stepper_rate(c4, G4, 100, use_graph=True, fused=True)
+    # one composed Newton iteration on 1e7 cells through the public calls
+    P = S.Problem(ctx, c4)
+    z = torch.empty(3 * G4, dtype=torch.float64, device="cuda")
+    S.BW_InitialCondition(P, S.NVector(ctx, z))
+    d, fI, r, dl = (torch.empty_like(z) for _ in range(4))
+    ewt = torch.full_like(z, 1e6)
+    Md = torch.empty(G4, 3, 3, dtype=torch.float64, device="cuda")
+    vz, vd, vf, vr, vdl, vw = (S.NVector(ctx, t) for t in (z, d, fI, r, dl, ewt))
+    M = S.SUNMatrix(ctx, Md)
+    S.BW_ReactionJacobian(P, vz, M)
+    S.SUNMatScaleAddI(-2e-3 / 3, M)
+    LS = S.SUNLinearSolver(vz, M)
+    S.SUNLinSolSetup(LS, M)
+    d.copy_(z)
+    c3 = [1.0, 2e-3 / 3, -1.0]
+
+    def newton_iter():
+        S.BW_ReactionRHS(P, vz, vf)
+        S.N_VLinearCombination(c3, [vd, vf, vz], vr)
+        S.SUNLinSolSolve(LS, M, vdl, vr)
+        S.N_VLinearSum(1.0, vz, 1.0, vdl, vz)
+        S.N_VWrmsNorm(vdl, vw)
+
+    newton_iter()
+    reps = 20
+    ms = timed(lambda: [newton_iter() for _ in range(reps)]) / reps
+    out["C4_1e7_reaction_cells"] = {
+        "fused_steps_per_s": round(r4, 1), "cell_steps_per_s": r4 * G4,
+        "composed_newton_iter_us": round(ms * 1e3, 1),
+        "composed_newton_iter_GB/s": round(388 * G4 / (ms * 1e-3) / 1e9, 1)}
+    del LS, M
+    P.destroy()
+    ctx.check("other configs")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -365,6 +443,10 @@ def main():
         del y0, yout, ydev
         torch.cuda.empty_cache()
         ops = nvector_ops(S, ctx, torch, peak)
+    configs = None
+    if rank == 0 and world == 1 and not args.no_ops:
+        torch.cuda.empty_cache()
+        configs = other_configs(S, ctx, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_sample()
@@ -384,7 +466,7 @@ def main():
             "roofline": roofline, "composed_equiv_bytes_per_step": step_bytes,
             "step_GB/s": round(step_bytes / (ms / args.steps * 1e-3) / 1e9, 1),
             "kernels": kernels, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "cpu_baseline": cpu, "nvector_ops_1e8": ops,
+            "cpu_baseline": cpu, "nvector_ops_1e8": ops, "other_configs": configs,
             "newton_iters": stats["newton_iters"],
         }
         print(json.dumps(line), flush=True)
