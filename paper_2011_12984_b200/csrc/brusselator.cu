@@ -326,14 +326,16 @@ int bw_jacobian(void* prob, const double* y, double* J) {
 }
 
 // halo exchange only (ring shift of the last plane to the right neighbour)
-int bw_halo(void* prob, const double* y) {
+int bw_halo_stream(void* prob, const double* y, cudaStream_t stream) {
   auto* P = (Prob*)prob;
   SUNBW_Context ctx = P->ctx;
   if (ctx_nranks(ctx) == 1 || P->p.reaction_only || P->p.kind == 1) return 0;
   const double* last = y + 3 * P->G - P->halo_len;
-  int e = ctx->comm->halo_shift(last, P->d_halo, (size_t)P->halo_len, ctx->stream);
+  int e = ctx->comm->halo_shift(last, P->d_halo, (size_t)P->halo_len, stream);
   return e ? ctx_set_err(ctx, e) : 0;
 }
+
+int bw_halo(void* prob, const double* y) { return bw_halo_stream(prob, y, ((Prob*)prob)->ctx->stream); }
 
 // stencil only (assumes bw_halo ran for this y when P > 1)
 int bw_advection_stencil(void* prob, const double* y, double* f) {

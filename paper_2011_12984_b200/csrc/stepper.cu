@@ -36,14 +36,18 @@ namespace sunbw {
 int bw_reaction(void* prob, const double* y, double* f);
 int bw_jacobian(void* prob, const double* y, double* J);
 int bw_halo(void* prob, const double* y);
+int bw_halo_stream(void* prob, const double* y, cudaStream_t stream);
 int bw_advection_stencil(void* prob, const double* y, double* f);
 int64_t bw_local_cells(void* prob);
 int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, double h,
                  double rtol, double atol, const double* y, const double* yp, const double* fE,
                  const double* fEp, double* z, double* partials, unsigned long long* d_first,
-                 int* nblocks_out, const FusedAdvection* adv);
+                 int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
                double* d_min, double* d_nu, int* d_err);
+int fused_fold_local(SUNBW_Context ctx, const double* partials, int nblocks, int K, double* pending);
+int fused_finalize_pending(SUNBW_Context ctx, double* pending, int K, int64_t nglobal, double* d_min,
+                           double* d_nu, int* d_err);
 }  // namespace sunbw
 
 namespace {
@@ -65,6 +69,12 @@ struct Stepper {
   int* d_err;            // 1: non-positive ewt denominator seen
   double* d_partials;    // fused mode per-CTA partials
   SUNLinearSolver gm = nullptr;   // linsol 1: SPGMR, block-LU preconditioner
+  // fused mode on P > 1 ranks: halo on a side stream overlapping the
+  // interior tiles; reductions deferred to the end of Advance (fixed K)
+  cudaStream_t side = nullptr;
+  cudaEvent_t evA = nullptr, evB = nullptr;
+  double* d_pending = nullptr;   // K + 2: local [min, sums], flag
+  bool deferred = false;
   int64_t step = 0;
   double t = 0.0;
   BW_StepperStats st{};
@@ -144,26 +154,56 @@ int enqueue_step(Stepper* S, bool first) {
   const double h = o.h;
   const double gamma = first ? h : (2.0 * h) / 3.0;
 
-  { Timed t(S, BW_K_HALO); TRY(sunbw::bw_halo(S->prob, y)); }
   sunbw::FusedAdvection fa;
   const bool adv_in_kernel = o.fused && o.fused_advection && sunbw::bw_fused_advection(S->prob, y, &fa) &&
                              G % 128 == 0;
-  if (!adv_in_kernel) {
-    Timed t(S, BW_K_ADVECTION);
-    TRY(sunbw::bw_advection_stencil(S->prob, y, fE));
+  // P > 1 with the single-kernel step: the halo plane travels on a side
+  // stream while the interior tiles (local planes k >= 1) are computed; the
+  // plane-0 tiles, which read it, run after the join (SURVEY §8(e) overlap)
+  const bool split = adv_in_kernel && ctx_nranks(ctx) > 1 && S->side;
+  if (!split) {
+    { Timed t(S, BW_K_HALO); TRY(sunbw::bw_halo(S->prob, y)); }
+    if (!adv_in_kernel) {
+      Timed t(S, BW_K_ADVECTION);
+      TRY(sunbw::bw_advection_stencil(S->prob, y, fE));
+    }
   }
 
   if (o.fused) {
-    int nb = 0;
-    {
+    int nb = 0, nb2 = 0;
+    if (split) {
+      const int64_t tpp = fa.nx * fa.ny / 128;          // tiles per z-plane
+      if (cudaEventRecord(S->evA, ctx->stream) != cudaSuccess ||
+          cudaStreamWaitEvent(S->side, S->evA, 0) != cudaSuccess)
+        return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      TRY(sunbw::bw_halo_stream(S->prob, y, S->side));
+      if (cudaEventRecord(S->evB, S->side) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      {
+        Timed t(S, BW_K_FUSED_NEWTON);
+        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
+                                S->d_partials, S->d_first, &nb, &fa, tpp, -1));
+      }
+      if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      {
+        Timed t(S, BW_K_FUSED_NEWTON);
+        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
+                                S->d_partials + (int64_t)nb * (o.K + 1), S->d_first, &nb2, &fa, 0, tpp));
+      }
+    } else {
       // with in-kernel advection fE is the f_E,n output (kept for the next
       // step's f_E,n-1), otherwise the input computed above
       Timed t(S, BW_K_FUSED_NEWTON);
       TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
-                              S->d_partials, S->d_first, &nb, adv_in_kernel ? &fa : nullptr));
+                              S->d_partials, S->d_first, &nb, adv_in_kernel ? &fa : nullptr, 0, -1));
     }
-    { Timed t(S, BW_K_WRMS); TRY(sunbw::fused_fold(ctx, S->d_partials, nb, o.K, S->nglobal, S->d_scal,
-                                                  S->d_scal + 1, S->d_err)); }
+    {
+      Timed t(S, BW_K_WRMS);
+      if (S->deferred)
+        TRY(sunbw::fused_fold_local(ctx, S->d_partials, nb + nb2, o.K, S->d_pending));
+      else
+        TRY(sunbw::fused_fold(ctx, S->d_partials, nb + nb2, o.K, S->nglobal, S->d_scal, S->d_scal + 1,
+                              S->d_err));
+    }
     return 0;
   }
 
@@ -244,6 +284,16 @@ int enqueue_step(Stepper* S, bool first) {
     }
   }
   return tol ? SUNBW_RECOV_NONCONV : 0;
+}
+
+// local (singular, bad-ewt) flags as doubles, and back after the allreduce
+__global__ void k_flags(const unsigned long long* first, const int* err, double* flags) {
+  flags[0] = *first != ~0ull ? 1.0 : 0.0;
+  flags[1] = *err ? 1.0 : 0.0;
+}
+__global__ void k_flags_back(const double* flags, unsigned long long* first, int* err) {
+  if (flags[0] != 0.0 && *first == ~0ull) *first = 0;   // singular elsewhere: report block 0
+  if (flags[1] != 0.0) *err = 1;
 }
 
 void rotate(Stepper* S) {
@@ -330,6 +380,14 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
     S->gm = sunbw::spgmr_create(ctx, G, 3, opt->maxl, true);
     if (!S->gm) e = SUNBW_ERR_MEM;
   }
+  if (!e && opt->fused && ctx_nranks(ctx) > 1) {
+    S->deferred = opt->newton_mode == 0;
+    if (cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S->evA, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S->evB, cudaEventDisableTiming) != cudaSuccess)
+      e = SUNBW_ERR_CUDA;
+    if (!e) e = alloc(S, &S->d_pending, kMaxK + 2);
+  }
   if (!e) e = alloc(S, &S->d_scal, kMaxK + 8);
   if (!e) e = alloc(S, &S->d_partials, (int64_t)(ctx->nsm * 16) * (kMaxK + 1));
   if (!e && cudaMalloc(&S->d_first, sizeof(unsigned long long)) != cudaSuccess) e = SUNBW_ERR_MEM;
@@ -355,6 +413,9 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
   SUNBW_Context ctx = S->ctx;
   if (y_out && (y_out->ctx != ctx || y_out->local_len != S->n)) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
   int rc = 0;
+  if (S->deferred &&
+      cudaMemsetAsync(S->d_pending + S->opt.K + 1, 0, sizeof(double), ctx->stream) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
   for (int64_t s = 0; s < nsteps; ++s) {
     bool first = S->step == 0;
     if (S->opt.use_graph && !first) {
@@ -384,6 +445,21 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
   unsigned long long f = 0;
   int err = 0;
   double nu = 0.0;
+  if (S->deferred && nsteps > 0) {
+    int e = sunbw::fused_finalize_pending(ctx, S->d_pending, S->opt.K, S->nglobal, S->d_scal,
+                                          S->d_scal + 1, S->d_err);
+    if (e) return e;
+  }
+  if (S->opt.newton_mode == 0 && ctx_nranks(ctx) > 1) {
+    // every rank returns the same code: OR the local flags over the ranks
+    double* flags = ctx->d_red + 96;
+    k_flags<<<1, 1, 0, ctx->stream>>>(S->d_first, S->d_err, flags);
+    ctx->launches++;
+    int e = ctx->comm->allreduce(flags, 2, RED_MAX, ctx->stream);
+    if (e) return ctx_set_err(ctx, e);
+    k_flags_back<<<1, 1, 0, ctx->stream>>>(flags, S->d_first, S->d_err);
+    ctx->launches++;
+  }
   if (S->opt.newton_mode == 0) {
     if (cudaMemcpyAsync(&f, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
         cudaMemcpyAsync(&err, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
@@ -449,6 +525,10 @@ extern "C" int BW_StepperDestroy(void* stepper) {
   if (S->d_first) cudaFree(S->d_first);
   if (S->d_err) cudaFree(S->d_err);
   if (S->gm) sunbw::spgmr_free(S->gm);
+  if (S->side) cudaStreamDestroy(S->side);
+  if (S->evA) cudaEventDestroy(S->evA);
+  if (S->evB) cudaEventDestroy(S->evB);
+  if (S->d_pending) cudaFree(S->d_pending);
   delete S;
   return 0;
 }
