@@ -325,3 +325,20 @@ def test_C4_full_size_1e7_cells(S, ctx):
         rc, y, _ = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=fused)
         assert rc == 0
         assert_bits_equal(y, yref, f"C4 1e7 fused={fused}")
+
+
+@pytest.mark.slow
+def test_C3_128cubed_ten_steps(S, ctx):
+    """C3 (3D, 128^3 cells, single B200): 10 steps of the composed path and
+    of the single-kernel fused step against the oracle on the whole state."""
+    n = 128
+    steps = 10
+    y0 = oracle.bruss_ic(n, n, n)
+    k = kappas(n, n, n)
+    _, yref, _, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=n, ny=n, nz=n,
+                                          kx=k[0], ky=k[1], kz=k[2], h=1e-3)
+    params = S.bruss_params(dim=3, nx=n, ny=n, nz=n)
+    for fused in (False, True):
+        rc, y, _ = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=fused, use_graph=True)
+        assert rc == 0
+        assert_bits_equal(y, yref, f"C3 128^3 fused={fused}")
