@@ -113,6 +113,13 @@ _SIGS = {
     "N_VLinearCombination": (_I, [_I, _P, _P, _P]),
     "N_VScaleAddMulti": (_I, [_I, _P, _P, _P, _P]),
     "N_VDotProdMulti": (_I, [_I, _P, _P, _P]),
+    "N_VLinearSumVectorArray": (_I, [_I, _D, _P, _D, _P, _P]),
+    "N_VScaleVectorArray": (_I, [_I, _P, _P, _P]),
+    "N_VConstVectorArray": (_I, [_I, _D, _P]),
+    "N_VWrmsNormVectorArray": (_I, [_I, _P, _P, _P]),
+    "N_VWrmsNormMaskVectorArray": (_I, [_I, _P, _P, _P, _P]),
+    "N_VScaleAddMultiVectorArray": (_I, [_I, _I, _P, _P, _P, _P]),
+    "N_VLinearCombinationVectorArray": (_I, [_I, _I, _P, _P, _P]),
     "SUNMatrix_B200BlockDiag": (_P, [_P, _I64, _I]),
     "SUNMatrix_B200BlockDiagMake": (_P, [_P, _I64, _I, _P]),
     "SUNMatrix_B200BlockDiag_Data": (_P, [_P]),
@@ -335,6 +342,50 @@ def N_VDotProdMulti(x: NVector, Y: Sequence[NVector]):
     return list(out)
 
 
+# ------------------------------------------------------ vector-array ops
+def N_VLinearSumVectorArray(a, X, b, Y, Z) -> int:
+    return lib().N_VLinearSumVectorArray(len(X), a, _vec_array(X), b, _vec_array(Y), _vec_array(Z))
+
+
+def N_VScaleVectorArray(c, X, Z) -> int:
+    return lib().N_VScaleVectorArray(len(X), _dbl_array(c), _vec_array(X), _vec_array(Z))
+
+
+def N_VConstVectorArray(c, Z) -> int:
+    return lib().N_VConstVectorArray(len(Z), c, _vec_array(Z))
+
+
+def N_VWrmsNormVectorArray(X, W):
+    out = (_D * len(X))()
+    if lib().N_VWrmsNormVectorArray(len(X), _vec_array(X), _vec_array(W), out):
+        raise SunbwError("N_VWrmsNormVectorArray failed")
+    return list(out)
+
+
+def N_VWrmsNormMaskVectorArray(X, W, idv):
+    out = (_D * len(X))()
+    if lib().N_VWrmsNormMaskVectorArray(len(X), _vec_array(X), _vec_array(W), idv, out):
+        raise SunbwError("N_VWrmsNormMaskVectorArray failed")
+    return list(out)
+
+
+def _vec_array_2d(rows):
+    inner = [_vec_array(r) for r in rows]
+    arr = (_P * len(rows))(*[C.cast(r, _P) for r in inner])
+    arr._keep = inner
+    return arr
+
+
+def N_VScaleAddMultiVectorArray(a, X, Y, Z) -> int:
+    return lib().N_VScaleAddMultiVectorArray(len(X), len(a), _dbl_array(a), _vec_array(X),
+                                             _vec_array_2d(Y), _vec_array_2d(Z))
+
+
+def N_VLinearCombinationVectorArray(c, X, Z) -> int:
+    return lib().N_VLinearCombinationVectorArray(len(Z), len(c), _dbl_array(c), _vec_array_2d(X),
+                                                 _vec_array(Z))
+
+
 # ------------------------------------------------------- block-diagonal + LU
 class SUNMatrix:
     """Block-diagonal matrix wrapping a (G, m, m) float64 CUDA tensor."""
@@ -396,9 +447,7 @@ class SUNLinearSolver:
             return torch.empty(0, dtype=torch.int32)
         ptr = lib().SUNLinSol_B200BatchedLU_Pivots(self.handle)
         torch.cuda.synchronize()
-        tmp = torch.empty(n, dtype=torch.int32, device="cuda")
-        _copy_device_ptr(ptr, tmp, n * 4)
-        return tmp.cpu()
+        return _device_view(ptr, (n,), "<i4").cpu()
 
     def __del__(self):
         try:
@@ -409,14 +458,17 @@ class SUNLinearSolver:
         self.handle = None
 
 
-def _copy_device_ptr(src_ptr: int, dst: torch.Tensor, nbytes: int):
-    """cudaMemcpy from a raw device pointer into a CUDA tensor."""
-    rt = C.CDLL("libcudart.so.12") if not hasattr(_copy_device_ptr, "_rt") else _copy_device_ptr._rt
-    _copy_device_ptr._rt = rt
-    rt.cudaMemcpy.argtypes = [_P, _P, C.c_size_t, C.c_int]
-    rc = rt.cudaMemcpy(_P(dst.data_ptr()), _P(src_ptr), nbytes, 3)   # DeviceToDevice
-    if rc != 0:
-        raise SunbwError(f"cudaMemcpy failed ({rc})")
+class _CudaArray:
+    """A raw device pointer exposed through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _device_view(ptr: int, shape, typestr: str) -> torch.Tensor:
+    """torch view of library-owned device memory (valid while the owner lives)."""
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr), device="cuda")
 
 
 def SUNLinSolSetup(S: SUNLinearSolver, A: SUNMatrix) -> int:
