@@ -33,10 +33,17 @@ using sunbw::split_for;
 constexpr int kU = sunbw::kU;
 
 
+// Kernels holding several 32-B vectors per operand in registers (reductions,
+// fused multi-vector ops) are compiled for 256-thread CTAs: a 1024-thread
+// bound would cap them at 64 registers and spill.  A larger policy block
+// size is clamped for them.
+constexpr int kMaxBlockWide = 256;
+
 // launch configuration from the vector's execution policy
 inline sunbw::LaunchCfg stream_cfg(SUNBW_Context ctx, const _N_Vector* pol,
-                                   int64_t work_items) {
+                                   int64_t work_items, int max_block = 1024) {
   int block = pol ? pol->block : 256;
+  if (block > max_block) block = max_block;
   int64_t need = (work_items + (int64_t)block * kU - 1) / ((int64_t)block * kU);
   if (need < 1) need = 1;
   int64_t grid;
@@ -106,10 +113,13 @@ __global__ void __launch_bounds__(1024) k_stream(SArgs<NIN, NOUT> a, int64_t n, 
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = tid; i < sp.head; i += nth) stream_scalar<Op, NIN, NOUT>(a, i, op);
   for (int64_t i = sp.tail0 + tid; i < n; i += nth) stream_scalar<Op, NIN, NOUT>(a, i, op);
-  for (int64_t v0 = tid; v0 < sp.nvec; v0 += nth * kU) {
-    d4 in[kU][NIN > 0 ? NIN : 1];
+  // single-input ops keep as many 32-B loads in flight per thread as the
+  // two-input ones
+  constexpr int U = NIN <= 1 ? 2 * kU : kU;
+  for (int64_t v0 = tid; v0 < sp.nvec; v0 += nth * U) {
+    d4 in[U][NIN > 0 ? NIN : 1];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       int64_t v = v0 + u * nth;
       if (v < sp.nvec) {
 #pragma unroll
@@ -117,7 +127,7 @@ __global__ void __launch_bounds__(1024) k_stream(SArgs<NIN, NOUT> a, int64_t n, 
       }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       int64_t v = v0 + u * nth;
       if (v < sp.nvec) {
         d4 out[NOUT];
@@ -221,7 +231,7 @@ struct RArgs {
 };
 
 template <int KIND>
-__global__ void __launch_bounds__(1024) k_reduce(RArgs a, int64_t n, Split sp, double* partials) {
+__global__ void __launch_bounds__(kMaxBlockWide) k_reduce(RArgs a, int64_t n, Split sp, double* partials) {
   using T = RedTraits<KIND>;
   constexpr int NIN = T::NIN;
   __shared__ double sh[32];
@@ -319,6 +329,7 @@ int launch_reduce(SUNBW_Context ctx, const _N_Vector* pol, int64_t n, RArgs a, s
                   int64_t nglobal, double* d_out, double* h_out, bool global) {
   using T = RedTraits<KIND>;
   int block = pol ? pol->reduce_block : 256;
+  if (block > kMaxBlockWide) block = kMaxBlockWide;
   Split sp = split_for(n, a.in, T::NIN);
   int64_t items = sp.nvec > 0 ? sp.nvec : n;
   int grid = reduce_grid(ctx, pol, items, block);
@@ -364,7 +375,7 @@ __device__ __forceinline__ double lc_elem(const double* xin, double zin, const d
 }
 
 template <int NV, bool ACC>
-__global__ void __launch_bounds__(1024) k_lincomb(FusedArgs a, int64_t n, Split sp) {
+__global__ void __launch_bounds__(kMaxBlockWide) k_lincomb(FusedArgs a, int64_t n, Split sp) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   double xin[NV];
@@ -396,7 +407,7 @@ __global__ void __launch_bounds__(1024) k_lincomb(FusedArgs a, int64_t n, Split 
 
 // Z_j = a_j x + Y_j
 template <int NV>
-__global__ void __launch_bounds__(1024) k_scaleaddmulti(FusedArgs a, int64_t n, Split sp) {
+__global__ void __launch_bounds__(kMaxBlockWide) k_scaleaddmulti(FusedArgs a, int64_t n, Split sp) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   auto scalar = [&](int64_t i) {
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(1024) k_scaleaddmulti(FusedArgs a, int64_t n, 
 
 // partial dots d_j = x·Y_j, one partial per CTA per j (stride NV)
 template <int NV>
-__global__ void __launch_bounds__(1024) k_dotmulti(FusedArgs a, int64_t n, Split sp, double* partials) {
+__global__ void __launch_bounds__(kMaxBlockWide) k_dotmulti(FusedArgs a, int64_t n, Split sp, double* partials) {
   using T = RedTraits<sunbw::RK_DOT>;
   __shared__ double sh[32];
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -467,7 +478,7 @@ int lincomb_chunk(SUNBW_Context ctx, const _N_Vector* pol, int64_t n, int nv, bo
   ptrs[nv] = a.z;
   Split sp = split_for(n, ptrs, nv + 1);
   int64_t items = sp.nvec > 0 ? sp.nvec : n;
-  sunbw::LaunchCfg cfg = stream_cfg(ctx, pol, items * kU);   // one vector per thread-iteration
+  sunbw::LaunchCfg cfg = stream_cfg(ctx, pol, items * kU, kMaxBlockWide);   // one vector per thread-iteration
   dim3 g(cfg.grid), b(cfg.block);
   cudaStream_t s = ctx->stream;
 #define LC_CASE(NV)                                                        \
@@ -490,7 +501,7 @@ int scaleaddmulti_chunk(SUNBW_Context ctx, const _N_Vector* pol, int64_t n, int 
   ptrs[2 * nv] = a.x;
   Split sp = split_for(n, ptrs, 2 * nv + 1);
   int64_t items = sp.nvec > 0 ? sp.nvec : n;
-  sunbw::LaunchCfg cfg = stream_cfg(ctx, pol, items * kU);
+  sunbw::LaunchCfg cfg = stream_cfg(ctx, pol, items * kU, kMaxBlockWide);
   dim3 g(cfg.grid), b(cfg.block);
   cudaStream_t s = ctx->stream;
 #define SAM_CASE(NV) case NV: k_scaleaddmulti<NV><<<g, b, 0, s>>>(a, n, sp); break;
@@ -511,6 +522,7 @@ int dotmulti_chunk(SUNBW_Context ctx, const _N_Vector* pol, int64_t n, int nv, F
   Split sp = split_for(n, ptrs, nv + 1);
   int64_t items = sp.nvec > 0 ? sp.nvec : n;
   int block = pol ? pol->reduce_block : 256;
+  if (block > kMaxBlockWide) block = kMaxBlockWide;
   int grid = reduce_grid(ctx, pol, items * kU, block);
   dim3 g(grid), b(block);
   cudaStream_t s = ctx->stream;
