@@ -42,10 +42,10 @@ int64_t bw_local_cells(void* prob);
 int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, double h,
                  double rtol, double atol, const double* y, const double* yp, const double* fE,
                  const double* fEp, double* z, double* partials, unsigned long long* d_first,
-                 int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end);
+                 int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end,
+                 const FusedFold* fold);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
                double* d_min, double* d_nu, int* d_err);
-int fused_fold_local(SUNBW_Context ctx, const double* partials, int nblocks, int K, double* pending);
 int fused_finalize_pending(SUNBW_Context ctx, double* pending, int K, int64_t nglobal, double* d_min,
                            double* d_nu, int* d_err);
 }  // namespace sunbw
@@ -68,6 +68,7 @@ struct Stepper {
   double* d_scal;        // [0] ewt min, [1..K] nu per iteration
   int* d_err;            // 1: non-positive ewt denominator seen
   double* d_partials;    // fused mode per-CTA partials
+  unsigned* d_counter = nullptr;   // fused mode: arrival counter of the in-kernel fold
   SUNLinearSolver gm = nullptr;   // linsol 1: SPGMR, block-LU preconditioner
   // fused mode on P > 1 ranks: halo on a side stream overlapping the
   // interior tiles; reductions deferred to the end of Advance (fixed K)
@@ -171,6 +172,12 @@ int enqueue_step(Stepper* S, bool first) {
 
   if (o.fused) {
     int nb = 0, nb2 = 0;
+    // partials are folded by the step's last CTA unless a blocking
+    // allreduce must sit between fold and finalisation (P > 1, not deferred)
+    const bool fold_in_kernel = S->deferred || ctx_nranks(ctx) <= 1;
+    sunbw::FusedFold fold{0, S->d_counter, S->deferred ? S->d_pending : nullptr, S->d_scal, S->d_scal + 1,
+                          S->d_err, S->nglobal};
+    const sunbw::FusedFold* fk = fold_in_kernel ? &fold : nullptr;
     if (split) {
       const int64_t tpp = fa.nx * fa.ny / 128;          // tiles per z-plane
       if (cudaEventRecord(S->evA, ctx->stream) != cudaSuccess ||
@@ -181,28 +188,27 @@ int enqueue_step(Stepper* S, bool first) {
       {
         Timed t(S, BW_K_FUSED_NEWTON);
         TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
-                                S->d_partials, S->d_first, &nb, &fa, tpp, -1));
+                                S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr));
       }
       if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      fold.prev_parts = nb;
       {
         Timed t(S, BW_K_FUSED_NEWTON);
         TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
-                                S->d_partials + (int64_t)nb * (o.K + 1), S->d_first, &nb2, &fa, 0, tpp));
+                                S->d_partials + (int64_t)nb * (o.K + 1), S->d_first, &nb2, &fa, 0, tpp,
+                                fk));
       }
     } else {
       // with in-kernel advection fE is the f_E,n output (kept for the next
       // step's f_E,n-1), otherwise the input computed above
       Timed t(S, BW_K_FUSED_NEWTON);
       TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
-                              S->d_partials, S->d_first, &nb, adv_in_kernel ? &fa : nullptr, 0, -1));
+                              S->d_partials, S->d_first, &nb, adv_in_kernel ? &fa : nullptr, 0, -1, fk));
     }
-    {
+    if (!fold_in_kernel) {
       Timed t(S, BW_K_WRMS);
-      if (S->deferred)
-        TRY(sunbw::fused_fold_local(ctx, S->d_partials, nb + nb2, o.K, S->d_pending));
-      else
-        TRY(sunbw::fused_fold(ctx, S->d_partials, nb + nb2, o.K, S->nglobal, S->d_scal, S->d_scal + 1,
-                              S->d_err));
+      TRY(sunbw::fused_fold(ctx, S->d_partials, nb + nb2, o.K, S->nglobal, S->d_scal, S->d_scal + 1,
+                            S->d_err));
     }
     return 0;
   }
@@ -392,6 +398,7 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   if (!e) e = alloc(S, &S->d_partials, (int64_t)(ctx->nsm * 16) * (kMaxK + 1));
   if (!e && cudaMalloc(&S->d_first, sizeof(unsigned long long)) != cudaSuccess) e = SUNBW_ERR_MEM;
   if (!e && cudaMalloc(&S->d_err, sizeof(int)) != cudaSuccess) e = SUNBW_ERR_MEM;
+  if (!e && cudaMalloc(&S->d_counter, sizeof(unsigned)) != cudaSuccess) e = SUNBW_ERR_MEM;
   if (e) {
     cudaGetLastError();
     BW_StepperDestroy(S);
@@ -399,7 +406,8 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   }
   if (cudaMemcpyAsync(S->y[S->iy], y0->d, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(S->d_first, 0xFF, sizeof(unsigned long long), ctx->stream) != cudaSuccess ||
-      cudaMemsetAsync(S->d_err, 0, sizeof(int), ctx->stream) != cudaSuccess) {
+      cudaMemsetAsync(S->d_err, 0, sizeof(int), ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(S->d_counter, 0, sizeof(unsigned), ctx->stream) != cudaSuccess) {
     BW_StepperDestroy(S);
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
   }
@@ -523,6 +531,7 @@ extern "C" int BW_StepperDestroy(void* stepper) {
     if (b) cudaFree(b);
   if (S->piv) cudaFree(S->piv);
   if (S->d_first) cudaFree(S->d_first);
+  if (S->d_counter) cudaFree(S->d_counter);
   if (S->d_err) cudaFree(S->d_err);
   if (S->gm) sunbw::spgmr_free(S->gm);
   if (S->side) cudaStreamDestroy(S->side);

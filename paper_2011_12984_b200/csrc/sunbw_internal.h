@@ -158,6 +158,20 @@ struct FusedAdvection {
 // the Newton kernel (3D Brusselator, nx % 128 == 0, ny > 1, nz > 1)
 bool bw_fused_advection(void* prob, const double* y, FusedAdvection* fa);
 
+// In-kernel fold of the fused step's per-CTA partials: the last CTA of the
+// step's final launch (self-resetting arrival counter) folds every partial
+// of the step in fixed order and writes either the finalised values (d_min,
+// d_nu, d_err; no communicator) or the local pending record (pending != 0).
+struct FusedFold {
+  int prev_parts;            // partial rows written by earlier launches of this step
+  unsigned* counter;         // zero-initialised
+  double* pending;           // K + 2: [min, sums], flag  (deferred mode)
+  double* d_min;
+  double* d_nu;
+  int* d_err;
+  int64_t nglobal;
+};
+
 }  // namespace sunbw
 
 #define SUNBW_CUDA_TRY(ctx, expr)                                \

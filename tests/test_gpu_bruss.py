@@ -199,6 +199,47 @@ def test_C4_reaction_only_cells(S, ctx):
         assert_bits_equal(y, yref, f"C4 fused={fused}")
 
 
+def _inject_extremes(y0, stream):
+    """Cells whose divisions leave the fused kernel's fast range: tiny
+    magnitudes (products below 2^-480), exact zeros and negative zeros."""
+    y = y0.copy().reshape(-1, 3)
+    G = y.shape[0]
+    u = synth.uniform(stream, G).numpy()
+    y[u < 0.03] *= 1e-160
+    y[(u >= 0.03) & (u < 0.05)] = 0.0
+    y[(u >= 0.05) & (u < 0.06), 0] = -0.0
+    y[(u >= 0.06) & (u < 0.07), 2] = 1e-300
+    return y.reshape(-1)
+
+
+def test_fused_guarded_divisions_fall_back_exactly(S, ctx):
+    """The fused kernel divides by Markstein steps on shared reciprocals and
+    recomputes a cell with IEEE divisions when any operand guard fails;
+    cells built to fail them (and ragged-tail cells) stay bit-identical to
+    the oracle, as do the composed kernels."""
+    G, steps = 100_003, 3
+    u = synth.uniform(synth.S_CELL, G, 0, 1).numpy()
+    y0 = np.stack([1.0 + 0.1 * u, 3.5 + 0.1 * u, 3.0 + 0.1 * u], 1).reshape(-1)
+    y0 = _inject_extremes(y0, 77)
+    params = S.bruss_params(dim=1, nx=G, reaction_only=True)
+    _, yref, _, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=G, reaction_only=True, h=1e-3)
+    for fused in (False, True):
+        _, y, _ = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=fused)
+        assert_bits_equal(y, yref, f"extreme cells fused={fused}")
+
+
+def test_fused_advection_guarded_divisions(S, ctx):
+    nx, ny, nz = 128, 4, 3
+    steps = 3
+    y0 = _inject_extremes(oracle.bruss_ic(nx, ny, nz), 78)
+    k = kappas(nx, ny, nz)
+    _, yref, _, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=nx, ny=ny, nz=nz,
+                                          kx=k[0], ky=k[1], kz=k[2], h=1e-3)
+    params = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz)
+    _, y, _ = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=True, use_graph=True)
+    assert_bits_equal(y, yref, "3D fused step with extreme cells")
+
+
 # ------------------------------------------------------ multi-rank (fake comm)
 def run_ranks(S, nranks, fn):
     comm = S.FakeComm(nranks)

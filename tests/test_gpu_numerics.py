@@ -59,3 +59,14 @@ def test_division_primitive_edge_mantissas(S, ctx):
     mism, checked = S.selftest_division(ctx, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
     assert checked >= A.size - 16          # a few scaled values leave [2^-480, 2^480)
     assert mism == 0
+
+
+def test_division_primitive_signed_zero_dividends(S, ctx):
+    """±0 / b inside the fast path (a converged Newton correction divides
+    zero by the pivot): the quotient keeps the IEEE sign, sign(a)·sign(b)."""
+    n = 1_000_000
+    b = rand_magnitudes(3, n).cuda()
+    a = torch.where(synth.uniform(4, n, device="cuda") < 0.5, 0.0, -0.0).double()
+    mism, checked = S.selftest_division(ctx, a, b)
+    assert checked == n
+    assert mism == 0
