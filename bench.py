@@ -32,12 +32,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # algorithmic HBM bytes per cell per launch, per kernel (DESIGN.md §6,
-# SURVEY §8(d)); the fused Newton kernel reads y_n, y_{n-1}, f_E,n, f_E,n-1
-# and writes y_{n+1} (72 B on the SBDF1 step)
+# SURVEY §8(d)); the fused Newton kernel reads y_n and the SBDF2 history H_n
+# and writes y_{n+1} and H_{n+1} (R28; y_n's row/plane neighbours for the
+# in-kernel advection are L2 hits, not counted)
 BYTES_PER_CELL = {
     "advection": 48, "rhs_combine": 120, "ewt": 216, "predict": 48, "jacobian": 96,
     "scaleaddi": 144, "lu_setup": 148, "reaction": 48, "residual": 96, "lu_solve": 124,
-    "update": 72, "wrms": 48, "fused_newton": 120, "halo": 0,
+    "update": 72, "wrms": 48, "fused_newton": 96, "halo": 0,
 }
 WRMS_FUSED_BYTES = 0        # the fused path's fold reads only per-CTA partials
 

@@ -520,9 +520,12 @@ int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
       oracle_linear_sum(n, 1.0, y, P->h, fE.data(), d.data());
       gamma = P->h;
     } else {
-      double c[4] = {4.0 / 3.0, -1.0 / 3.0, (4.0 * P->h) / 3.0,
-                     -((2.0 * P->h) / 3.0)};
-      const double* X[4] = {y, yprev.data(), fE.data(), fEprev.data()};
+      // SBDF2 (P:384-385 IMEX split; R14 coefficients), d = 4/3 y_n - 1/3 y_{n-1}
+      // + 4h/3 f_E,n - 2h/3 f_E,n-1, as one LinearCombination with the
+      // history terms first (R28: the paper fixes no summation order)
+      double c[4] = {-1.0 / 3.0, -((2.0 * P->h) / 3.0), 4.0 / 3.0,
+                     (4.0 * P->h) / 3.0};
+      const double* X[4] = {yprev.data(), fEprev.data(), y, fE.data()};
       oracle_linear_combination(4, c, X, n, d.data());
       gamma = (2.0 * P->h) / 3.0;
     }

@@ -40,8 +40,8 @@ int bw_halo_stream(void* prob, const double* y, cudaStream_t stream);
 int bw_advection_stencil(void* prob, const double* y, double* f);
 int64_t bw_local_cells(void* prob);
 int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, double h,
-                 double rtol, double atol, const double* y, const double* yp, const double* fE,
-                 const double* fEp, double* z, double* partials, unsigned long long* d_first,
+                 double rtol, double atol, const double* y, const double* fE, const double* hin,
+                 double* hout, double* z, double* partials, unsigned long long* d_first,
                  int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end,
                  const FusedFold* fold);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
@@ -162,11 +162,15 @@ int enqueue_step(Stepper* S, bool first) {
   // stream while the interior tiles (local planes k >= 1) are computed; the
   // plane-0 tiles, which read it, run after the join (SURVEY §8(e) overlap)
   const bool split = adv_in_kernel && ctx_nranks(ctx) > 1 && S->side;
+  // fused mode: fE[ife] / fE[ifep] hold the SBDF2 history H_{n+1} / H_n
+  // (R28) and y[iyp] (y_{n-1}, unused) takes f_E,n when it is computed by
+  // the separate stencil kernel
+  double* fE_n = o.fused ? yp : fE;
   if (!split) {
     { Timed t(S, BW_K_HALO); TRY(sunbw::bw_halo(S->prob, y)); }
     if (!adv_in_kernel) {
       Timed t(S, BW_K_ADVECTION);
-      TRY(sunbw::bw_advection_stencil(S->prob, y, fE));
+      TRY(sunbw::bw_advection_stencil(S->prob, y, fE_n));
     }
   }
 
@@ -187,23 +191,22 @@ int enqueue_step(Stepper* S, bool first) {
       if (cudaEventRecord(S->evB, S->side) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
       {
         Timed t(S, BW_K_FUSED_NEWTON);
-        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
+        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
                                 S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr));
       }
       if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
       fold.prev_parts = nb;
       {
         Timed t(S, BW_K_FUSED_NEWTON);
-        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
+        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
                                 S->d_partials + (int64_t)nb * (o.K + 1), S->d_first, &nb2, &fa, 0, tpp,
                                 fk));
       }
     } else {
-      // with in-kernel advection fE is the f_E,n output (kept for the next
-      // step's f_E,n-1), otherwise the input computed above
       Timed t(S, BW_K_FUSED_NEWTON);
-      TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, yp, fE, fEp, z,
-                              S->d_partials, S->d_first, &nb, adv_in_kernel ? &fa : nullptr, 0, -1, fk));
+      TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y,
+                              adv_in_kernel ? nullptr : fE_n, fEp, fE, z, S->d_partials, S->d_first, &nb,
+                              adv_in_kernel ? &fa : nullptr, 0, -1, fk));
     }
     if (!fold_in_kernel) {
       Timed t(S, BW_K_WRMS);
@@ -218,8 +221,9 @@ int enqueue_step(Stepper* S, bool first) {
     if (first) {
       TRY(sunbw::linear_sum(ctx, n, 1.0, y, h, fE, S->d, nullptr));
     } else {
-      const double c[4] = {4.0 / 3.0, -1.0 / 3.0, (4.0 * h) / 3.0, -((2.0 * h) / 3.0)};
-      const double* X[4] = {y, yp, fE, fEp};
+      // history terms first (R28): the fused kernel carries their sum
+      const double c[4] = {-1.0 / 3.0, -((2.0 * h) / 3.0), 4.0 / 3.0, (4.0 * h) / 3.0};
+      const double* X[4] = {yp, fEp, y, fE};
       TRY(sunbw::linear_combination(ctx, n, 4, c, X, S->d, nullptr));
     }
   }
