@@ -383,3 +383,26 @@ def test_C3_128cubed_ten_steps(S, ctx):
         rc, y, _ = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=3, fused=fused, use_graph=True)
         assert rc == 0
         assert_bits_equal(y, yref, f"C3 128^3 fused={fused}")
+
+
+def test_fused_pivoting_cells_fall_back_exactly(S, ctx):
+    """The fused kernel's fast path factors without row exchanges and sends a
+    cell whose Newton matrix needs partial pivoting (|a_ik| > |a_kk|) to the
+    exact path, which pivots (first-maximum rule, O6).  Large steps on
+    random states make a sizeable fraction of the blocks pivot; the state
+    stays bit-identical to the oracle."""
+    G, steps, h = 50_001, 3, 0.1
+    u = synth.uniform(synth.S_CELL, G, 0.2, 2.0).numpy()
+    v = synth.uniform(synth.S_CELL + 10, G, 0.2, 3.0).numpy()
+    w = synth.uniform(synth.S_CELL + 11, G, 0.2, 3.0).numpy()
+    y0 = np.stack([u, v, w], 1).reshape(-1)
+    M = np.eye(3)[None] - h * oracle.bruss_jacobian(y0)
+    _, piv, _ = oracle.lu_factor(M)
+    assert np.mean(np.any(piv != np.arange(3)[None], axis=1)) > 0.01   # the test exercises pivoting
+    params = S.bruss_params(dim=1, nx=G, reaction_only=True)
+    rc2, yref, _, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=G, reaction_only=True, h=h)
+    assert rc2 == 0
+    for fused in (False, True):
+        rc, y, _ = run_gpu(S, ctx, params, y0, steps, h=h, K=3, fused=fused)
+        assert rc == 0
+        assert_bits_equal(y, yref, f"pivoting cells fused={fused}")
