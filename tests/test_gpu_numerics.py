@@ -62,11 +62,14 @@ def test_division_primitive_edge_mantissas(S, ctx):
 
 
 def test_division_primitive_signed_zero_dividends(S, ctx):
-    """±0 / b inside the fast path (a converged Newton correction divides
-    zero by the pivot): the quotient keeps the IEEE sign, sign(a)·sign(b)."""
+    """+0 / b inside the fast path (a converged Newton correction divides
+    zero by the pivot): the quotient keeps the IEEE sign, sign(b); -0
+    dividends leave the fast path (the guard sends the cell to IEEE
+    division), so only the +0 half is checked."""
     n = 1_000_000
     b = rand_magnitudes(3, n).cuda()
-    a = torch.where(synth.uniform(4, n, device="cuda") < 0.5, 0.0, -0.0).double()
+    neg = synth.uniform(4, n, device="cuda") < 0.5
+    a = torch.where(neg, -0.0, 0.0).double()
     mism, checked = S.selftest_division(ctx, a, b)
-    assert checked == n
+    assert checked == n - int(neg.sum())
     assert mism == 0
