@@ -60,7 +60,8 @@ def test_reaction_and_jacobian_bit_exact(S, ctx):
     P.destroy()
 
 
-@pytest.mark.parametrize("shape", [(64, 1, 1), (1000, 1, 1), (16, 12, 8), (33, 7, 5), (64, 64, 32)])
+@pytest.mark.parametrize("shape", [(64, 1, 1), (1000, 1, 1), (16, 12, 8), (33, 7, 5), (64, 64, 32),
+                                   (10, 1, 6), (6, 5, 1), (256, 4, 3)])
 def test_advection_and_ic(S, ctx, shape):
     nx, ny, nz = shape
     dim = 1 if ny == nz == 1 else 3
