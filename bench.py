@@ -41,6 +41,16 @@ BYTES_PER_CELL = {
     "update": 72, "wrms": 48, "fused_newton": 96, "halo": 0,
 }
 WRMS_FUSED_BYTES = 0        # the fused path's fold reads only per-CTA partials
+NUM_SMS = 148
+FP64_LANES_PER_SM = 64
+
+
+def sm_max_mhz():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f).get("sm_max_mhz", 1965.0))
+    except (OSError, ValueError):
+        return 1965.0
 
 
 def measured_peak():
@@ -409,11 +419,25 @@ def main():
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                 else "fallback (B200_PROFILING.md)",
                 "bytes_per_launch": BYTES_PER_CELL[dom] * G}
-    # composed-path equivalent bytes: what the same step costs through the ABI
+    if fused and n_ax == 256 and os.path.exists(tpath):
+        # the fused step is as much an fp64-ALU kernel as an HBM one
+        # (DESIGN.md §6): its fp64-pipe instructions per cell (ncu, same
+        # workload) against 148 SMs x 64 FP64 lanes x the max SM clock
+        with open(tpath) as f:
+            ops = json.load(f).get("fused_newton_fp64_per_cell")
+        if ops:
+            a64 = ops * G / (kernels[dom]["us_avg"] * 1e-6) / 1e12
+            p64 = FP64_LANES_PER_SM * NUM_SMS * sm_max_mhz() * 1e6 / 1e12
+            roofline["fp64"] = {"achieved": round(a64, 2), "peak": round(p64, 2), "unit": "Top/s",
+                                "frac": round(a64 / p64, 4), "ops_per_cell": ops,
+                                "peak_source": "148 SMs x 64 FP64 lanes/clk (profiles/r01d_fp64_latency.txt: "
+                                               "0.49 fp64 warp-instr/clk/SMSP) x sm_max_mhz"}
+    # bytes per step of this mode; the composed path's are SURVEY §8(d)'s
+    # 820 + 388 K per cell, the fused step's 96 per cell (R28)
     step_bytes = sum(BYTES_PER_CELL[k] * G * v["launches"] for k, v in kernels.items()
                      if BYTES_PER_CELL.get(k)) / args.steps
     if fused:
-        step_bytes = (BYTES_PER_CELL["fused_newton"] + BYTES_PER_CELL["advection"]) * G
+        step_bytes = BYTES_PER_CELL["fused_newton"] * G
 
     # e2e through the public API with host buffers: pinned H2D of the initial
     # state, Advance(K), D2H of the final state (per-step bytes = state/K)
@@ -464,7 +488,7 @@ def main():
                        "cells_per_gpu": G, "global_grid": [n_ax, n_ax, n_ax * world],
                        "K": 3, "h": 1e-3, "mode": args.mode, "parallelism": f"z-slab x{world}",
                        "l2": "inputs larger than L2 (state 403 MB per vector)"},
-            "roofline": roofline, "composed_equiv_bytes_per_step": step_bytes,
+            "roofline": roofline, "step_bytes": step_bytes, "composed_equiv_bytes_per_step": (820 + 388 * 3) * G,
             "step_GB/s": round(step_bytes / (ms / args.steps * 1e-3) / 1e9, 1),
             "kernels": kernels, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "cpu_baseline": cpu, "nvector_ops_1e8": ops, "other_configs": configs,
