@@ -39,6 +39,7 @@ int bw_halo(void* prob, const double* y);
 int bw_halo_stream(void* prob, const double* y, cudaStream_t stream);
 int bw_advection_stencil(void* prob, const double* y, double* f);
 int64_t bw_local_cells(void* prob);
+BW_BrussParams bw_params(void* prob);
 int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, double h,
                  double rtol, double atol, const double* y, const double* fE, const double* hin,
                  double* hout, double* z, double* partials, unsigned long long* d_first,
@@ -166,9 +167,12 @@ int enqueue_step(Stepper* S, bool first) {
   // (R28) and y[iyp] (y_{n-1}, unused) takes f_E,n when it is computed by
   // the separate stencil kernel
   double* fE_n = o.fused ? yp : fE;
+  // fused step of a reaction-only problem: f_E ≡ 0 is not materialised
+  const bool fzero = o.fused && !adv_in_kernel && sunbw::bw_params(S->prob).reaction_only;
+  if (fzero) fE_n = nullptr;
   if (!split) {
     { Timed t(S, BW_K_HALO); TRY(sunbw::bw_halo(S->prob, y)); }
-    if (!adv_in_kernel) {
+    if (!adv_in_kernel && !fzero) {
       Timed t(S, BW_K_ADVECTION);
       TRY(sunbw::bw_advection_stencil(S->prob, y, fE_n));
     }
