@@ -199,6 +199,55 @@ __global__ void __launch_bounds__(256) k_adv3d(const double* __restrict__ y,
   }
 }
 
+// Multi-row variant: a CTA of 256 threads takes RPB consecutive rows, each
+// thread EPT values per row (3·nx <= 256·EPT); all of a thread's loads are
+// issued before any value is used (RPB·EPT independent y_n loads in flight
+// per thread instead of one).  Same arithmetic and order as k_adv3d.
+template <int RPB, int EPT>
+__global__ void __launch_bounds__(256) k_adv3d_r(const double* __restrict__ y,
+                                                 const double* __restrict__ below,
+                                                 double* __restrict__ f, Adv3 a) {
+  const int rowlen = 3 * a.nx;
+  const int64_t plane = (int64_t)rowlen * a.ny;
+  const int nrows = a.ny * a.nzl;
+  for (int r0 = blockIdx.x * RPB; r0 < nrows; r0 += gridDim.x * RPB) {
+    double q[RPB][EPT], qx[RPB][EPT], qy[RPB][EPT], qz[RPB][EPT];
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr) {
+      const int r = r0 + rr < nrows ? r0 + rr : nrows - 1;
+      const int j = r % a.ny, k = r / a.ny;
+      const int64_t base = (int64_t)r * rowlen;
+      const int64_t rowm = j > 0 ? base - rowlen : base + (int64_t)(a.ny - 1) * rowlen;
+      const double* zrow = k > 0 ? y + base - plane : below + (int64_t)j * rowlen;
+#pragma unroll
+      for (int c = 0; c < EPT; ++c) {
+        int e = threadIdx.x + 256 * c;
+        e = e < rowlen ? e : rowlen - 1;
+        const int em = e >= 3 ? e - 3 : e + rowlen - 3;
+        q[rr][c] = __ldg(y + base + e);
+        qx[rr][c] = __ldg(y + base + em);
+        qy[rr][c] = a.ny_g > 1 ? __ldg(y + rowm + e) : 0.0;
+        qz[rr][c] = a.nz_g > 1 ? __ldg(zrow + e) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr) {
+      const int r = r0 + rr;
+      if (r >= nrows) break;
+      const int64_t base = (int64_t)r * rowlen;
+#pragma unroll
+      for (int c = 0; c < EPT; ++c) {
+        const int e = threadIdx.x + 256 * c;
+        if (e >= rowlen) break;
+        double acc = __dmul_rn(a.kx, __dsub_rn(qx[rr][c], q[rr][c]));
+        if (a.ny_g > 1) acc = __dadd_rn(acc, __dmul_rn(a.ky, __dsub_rn(qy[rr][c], q[rr][c])));
+        if (a.nz_g > 1) acc = __dadd_rn(acc, __dmul_rn(a.kz, __dsub_rn(qz[rr][c], q[rr][c])));
+        f[base + e] = acc;
+      }
+    }
+  }
+}
+
 // Vectorised 3D variant for 3·nx % 4 == 0 (nx % 4 == 0) and 32-B aligned
 // rows: thread v owns the 4 values [4v, 4v+4) of the row; the row is staged
 // in shared memory for the x-neighbour (e-3 crosses 32-B vectors), the y-1
@@ -362,7 +411,19 @@ int bw_advection_stencil(void* prob, const double* y, double* f) {
 #endif
     const bool vec = SUNBW_ADV_VARIANT > 0 && rowlen % 4 == 0 && rowlen <= 2048 &&
                      (((uintptr_t)y | (uintptr_t)f | (uintptr_t)left) & 31) == 0;
-    if (vec) {
+#ifndef SUNBW_ADV_RPB
+#define SUNBW_ADV_RPB 2
+#endif
+    if (SUNBW_ADV_RPB > 0 && rowlen <= 4 * 256 && !vec) {
+      constexpr int R = SUNBW_ADV_RPB > 0 ? SUNBW_ADV_RPB : 1;
+      const int ept = (rowlen + 255) / 256;
+      const int64_t need = (rows + R - 1) / R, cap = (int64_t)ctx->nsm * 8 * 4;
+      const int grid = (int)(need < cap ? need : cap);
+      if (ept == 1) k_adv3d_r<R, 1><<<grid, 256, 0, ctx->stream>>>(y, left, f, a);
+      else if (ept == 2) k_adv3d_r<R, 2><<<grid, 256, 0, ctx->stream>>>(y, left, f, a);
+      else if (ept == 3) k_adv3d_r<R, 3><<<grid, 256, 0, ctx->stream>>>(y, left, f, a);
+      else k_adv3d_r<R, 4><<<grid, 256, 0, ctx->stream>>>(y, left, f, a);
+    } else if (vec) {
       int nv = rowlen / 4;
       int block = nv <= 256 ? ((nv + 31) / 32) * 32 : 256;
       int64_t cap = SUNBW_ADV_VARIANT == 1 ? (int64_t)ctx->nsm * (2048 / block) : rows;
