@@ -14,4 +14,4 @@ echo "racecheck rc=$?" >> gpurun_out/sanitizer_racecheck.log
 timeout 600 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest -q -p no:cacheprovider \
   tests/test_gpu_bruss.py -k "3D_fused_step_kernel and shape2" > gpurun_out/sanitizer_synccheck.log 2>&1
 echo "synccheck rc=$?" >> gpurun_out/sanitizer_synccheck.log
-tail -3 gpurun_out/sanitizer_*.log
+for f in gpurun_out/sanitizer_*.log; do tail -3 $f; done
