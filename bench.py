@@ -364,7 +364,7 @@ def main():
     yout = torch.empty_like(y0)
     vyout = S.NVector(ctx, yout)
     fused = args.mode == "fused"
-    st = S.Stepper(P, vy0, S.stepper_options(h=1e-3, K=3, use_graph=False, timing=True, fused=fused))
+    st = S.Stepper(P, vy0, S.stepper_options(h=1e-3, K=3, use_graph=True, timing=True, fused=fused))
     rc, _ = st.advance(args.warmup)
     assert rc == 0, rc
     st.kernel_times(reset=True)

@@ -84,6 +84,12 @@ struct Stepper {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t gexec[6] = {};
   int64_t graph_launches[6] = {};
+  // timing mode with graphs: the captured graph's event-record nodes (in
+  // capture order, start/end pairs) get fresh pool events before each replay
+  cudaGraph_t graph[6] = {};
+  std::vector<cudaGraphNode_t> ev_nodes[6];
+  std::vector<int> ev_node_kind[6];
+  bool capturing = false;
   // timing
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -114,11 +120,13 @@ struct Timed {
         S->ev_pool.push_back(e);
       }
     }
-    cudaEventRecord(S->ev_pool[S->ev_used], S->ctx->stream);
+    cudaEventRecordWithFlags(S->ev_pool[S->ev_used], S->ctx->stream,
+                             S->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
   ~Timed() {
     if (!on) return;
-    cudaEventRecord(S->ev_pool[S->ev_used + 1], S->ctx->stream);
+    cudaEventRecordWithFlags(S->ev_pool[S->ev_used + 1], S->ctx->stream,
+                             S->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     S->ev_kind.push_back(kind);
     S->ev_used += 2;
   }
@@ -171,7 +179,10 @@ int enqueue_step(Stepper* S, bool first) {
   const bool fzero = o.fused && !adv_in_kernel && sunbw::bw_params(S->prob).reaction_only;
   if (fzero) fE_n = nullptr;
   if (!split) {
-    { Timed t(S, BW_K_HALO); TRY(sunbw::bw_halo(S->prob, y)); }
+    if (ctx_nranks(ctx) > 1) {   // one rank: periodic wrap in place, nothing to time
+      Timed t(S, BW_K_HALO);
+      TRY(sunbw::bw_halo(S->prob, y));
+    }
     if (!adv_in_kernel && !fzero) {
       Timed t(S, BW_K_ADVECTION);
       TRY(sunbw::bw_advection_stencil(S->prob, y, fE_n));
@@ -328,15 +339,43 @@ int capture_step(Stepper* S, int key) {
   ctx->stream = S->cap_stream;
   int64_t l0 = ctx->launches.load();
   int64_t it0 = S->st.newton_iters, so0 = S->st.solves;
+  const size_t ev0 = S->ev_used, kind0 = S->ev_kind.size();
   cudaGraph_t g = nullptr;
   int rc = 0;
   if (cudaStreamBeginCapture(S->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     rc = SUNBW_ERR_CUDA;
   } else {
+    S->capturing = true;
     rc = enqueue_step(S, false);
+    S->capturing = false;
     if (cudaStreamEndCapture(S->cap_stream, &g) != cudaSuccess) rc = rc ? rc : SUNBW_ERR_CUDA;
   }
   ctx->stream = user;
+  if (!rc && g && S->opt.timing) {
+    // event-record nodes in capture order: match each node's event with the
+    // pool entries the capture consumed
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    const size_t nev = S->ev_used - ev0;
+    std::vector<cudaGraphNode_t> ordered(nev, nullptr);
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      cudaGraphNodeGetType(nd, &ty);
+      if (ty != cudaGraphNodeTypeEventRecord) continue;
+      cudaEvent_t ev;
+      cudaGraphEventRecordNodeGetEvent(nd, &ev);
+      for (size_t i = 0; i < nev; ++i)
+        if (S->ev_pool[ev0 + i] == ev) ordered[i] = nd;
+    }
+    for (cudaGraphNode_t nd : ordered)
+      if (!nd) rc = SUNBW_ERR_CUDA;
+    S->ev_nodes[key] = ordered;
+    S->ev_node_kind[key].assign(S->ev_kind.begin() + kind0, S->ev_kind.end());
+    S->ev_used = ev0;                      // the capture's events measured nothing
+    S->ev_kind.resize(kind0);
+  }
   S->st.newton_iters = it0;
   S->st.solves = so0;
   S->graph_launches[key] = ctx->launches.load() - l0;
@@ -350,7 +389,7 @@ int capture_step(Stepper* S, int key) {
     cudaGraphDestroy(g);
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
   }
-  cudaGraphDestroy(g);
+  S->graph[key] = g;                       // kept: its event nodes are updated per replay
   return 0;
 }
 
@@ -371,7 +410,7 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   S->prob = prob;
   S->ctx = ctx;
   S->opt = *opt;
-  if (S->opt.timing || (ctx->comm && !ctx->comm->capturable())) S->opt.use_graph = 0;
+  if (ctx->comm && !ctx->comm->capturable()) S->opt.use_graph = 0;
   if (S->opt.newton_mode == 1 || S->opt.linsol == 1) S->opt.use_graph = 0;   // host decisions
   S->G = G;
   S->n = 3 * G;
@@ -439,6 +478,22 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
       if (!S->gexec[key]) {
         int e = capture_step(S, key);
         if (e) return e;
+      }
+      if (S->opt.timing && !S->ev_nodes[key].empty()) {
+        const std::vector<cudaGraphNode_t>& nodes = S->ev_nodes[key];
+        while (S->ev_used + nodes.size() > S->ev_pool.size()) {
+          for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            S->ev_pool.push_back(e);
+          }
+        }
+        for (size_t j = 0; j < nodes.size(); ++j)
+          if (cudaGraphExecEventRecordNodeSetEvent(S->gexec[key], nodes[j], S->ev_pool[S->ev_used + j]) !=
+              cudaSuccess)
+            return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+        S->ev_used += nodes.size();
+        S->ev_kind.insert(S->ev_kind.end(), S->ev_node_kind[key].begin(), S->ev_node_kind[key].end());
       }
       if (cudaGraphLaunch(S->gexec[key], ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
       ctx->launches += S->graph_launches[key];
@@ -531,6 +586,8 @@ extern "C" int BW_StepperDestroy(void* stepper) {
   cudaStreamSynchronize(S->ctx->stream);
   for (auto& g : S->gexec)
     if (g) cudaGraphExecDestroy(g);
+  for (auto& g : S->graph)
+    if (g) cudaGraphDestroy(g);
   if (S->cap_stream) cudaStreamDestroy(S->cap_stream);
   for (auto e : S->ev_pool) cudaEventDestroy(e);
   double* bufs[] = {S->y[0], S->y[1], S->y[2], S->fE[0], S->fE[1], S->d, S->ewt, S->tmp,
