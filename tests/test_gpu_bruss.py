@@ -407,3 +407,24 @@ def test_fused_pivoting_cells_fall_back_exactly(S, ctx):
         rc, y, _ = run_gpu(S, ctx, params, y0, steps, h=h, K=3, fused=fused)
         assert rc == 0
         assert_bits_equal(y, yref, f"pivoting cells fused={fused}")
+
+
+@pytest.mark.parametrize("K", [1, 2, 4, 8])
+@pytest.mark.parametrize("shape", [(128, 3, 2), (300, 1, 1)])
+def test_fused_newton_iteration_counts(S, ctx, K, shape):
+    """The fused step for every compile-time K other than the bench's 3 (the
+    Newton loop is unrolled per K; K = 1 forms the WRMS partial in its only
+    iteration), 3D with in-kernel advection and 1D with the stencil kernel
+    and a ragged tail: bit-identical states, ν to 1e-12."""
+    nx, ny, nz = shape
+    dim = 1 if ny == nz == 1 else 3
+    steps = 4
+    y0 = oracle.bruss_ic(nx, ny, nz)
+    k = kappas(nx, ny, nz)
+    _, yref, stref, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=K, nx=nx, ny=ny, nz=nz,
+                                              kx=k[0], ky=k[1], kz=k[2], h=1e-3)
+    params = S.bruss_params(dim=dim, nx=nx, ny=ny, nz=nz)
+    rc, y, stats = run_gpu(S, ctx, params, y0, steps, h=1e-3, K=K, fused=True, use_graph=True)
+    assert rc == 0 and stats["newton_iters"] == K * steps
+    assert_bits_equal(y, yref, f"fused K={K} {shape}")
+    assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-12 * stref["last_nu"]
