@@ -95,6 +95,8 @@ def lib():
             "oracle_dot_prod_multi": (None, [C.c_int, _P, _P, _I64, _P]),
             "oracle_scale_add_identity": (None, [_I64, C.c_int, _D, _P]),
             "oracle_lu_factor": (_I64, [_I64, C.c_int, _P, _P]),
+            "oracle_gj_inverse": (_I64, [_I64, C.c_int, _P, _P]),
+            "oracle_gj_apply": (None, [_I64, C.c_int, _P, _P, _P]),
             "oracle_lu_solve": (None, [_I64, C.c_int, _P, _P, _P, _P]),
             "oracle_block_matvec": (None, [_I64, C.c_int, _P, _P, _P]),
             "oracle_bruss_reaction": (None, [_I64, _P, _D, _D, _D, _P]),
@@ -248,6 +250,25 @@ def lu_factor(A):
     piv = np.zeros((G, m), dtype=np.int32)
     flag = lib().oracle_lu_factor(G, m, _ptr(LU), _ptr(piv))
     return LU, piv, int(flag)
+
+
+def gj_inverse(A):
+    """Block inverses by symbolic Gauss-Jordan without pivoting:
+    returns (Ainv (G,m,m), flag = 1 + first block with a zero pivot, else 0)."""
+    A = _f64(A)
+    G, m, _ = A.shape
+    B = np.empty_like(A)
+    flag = lib().oracle_gj_inverse(G, m, _ptr(A), _ptr(B))
+    return B, int(flag)
+
+
+def gj_apply(Ainv, b):
+    Ainv = _f64(Ainv)
+    G, m, _ = Ainv.shape
+    b = _f64(b).reshape(G * m)
+    x = np.empty_like(b)
+    lib().oracle_gj_apply(G, m, _ptr(Ainv), _ptr(b), _ptr(x))
+    return x
 
 
 def lu_solve(LU, piv, b):

@@ -251,6 +251,84 @@ int64_t oracle_lu_factor(int64_t G, int m, double* A, int32_t* piv) {
   return first_singular;
 }
 
+// Block inverse by symbolic Gauss-Jordan (the paper's task-local solver,
+// "applying the inverse of each 3x3 block matrix ... generated
+// offline with a symbolic Gauss-Jordan method").  Gauss-Jordan on [A | I]
+// WITHOUT pivoting (a symbolic elimination fixes the operation sequence),
+// k = 0..m-1 in order:
+//   p = RN(1/A_kk)                                 (pivot reciprocal)
+//   A_kj = RN(A_kj p), j > k;  B_kj = RN(B_kj p)   (normalise the pivot row)
+//   for i != k, f = A_ik:  A_ij = RN(A_ij - RN(f A_kj)), j > k
+//                          B_ij = RN(B_ij - RN(f B_kj))
+// "Symbolic": the right-hand block starts as the identity and the generator
+// emits no operation on its structural zeros and ones — B_kj = 0 is not
+// scaled or subtracted, a structural 1 times p is p, and 0 - RN(f B_kj) is
+// -RN(f B_kj).  The left block is treated as dense.  B ends as A^{-1}.
+// A zero pivot marks the block singular (first one returned, 1-based) and
+// the sequence continues with IEEE arithmetic (1/0 = inf).
+int64_t oracle_gj_inverse(int64_t G, int m, const double* Ain, double* Binv) {
+  int64_t first_singular = 0;
+  std::vector<double> A(m * m), B(m * m);
+  std::vector<int> kind(m * m);   // B structure: 0 structural zero, 1 structural one, 2 value
+  for (int64_t g = 0; g < G; ++g) {
+    for (int e = 0; e < m * m; ++e) {
+      A[e] = Ain[g * m * m + e];
+      B[e] = (e % (m + 1) == 0) ? 1.0 : 0.0;
+      kind[e] = (e % (m + 1) == 0) ? 1 : 0;
+    }
+    for (int k = 0; k < m; ++k) {
+      if (A[k * m + k] == 0.0 && first_singular == 0) first_singular = g + 1;
+      const double p = 1.0 / A[k * m + k];
+      for (int j = k + 1; j < m; ++j) A[k * m + j] = A[k * m + j] * p;
+      for (int j = 0; j < m; ++j) {
+        if (kind[k * m + j] == 0) continue;
+        B[k * m + j] = kind[k * m + j] == 1 ? p : B[k * m + j] * p;
+        kind[k * m + j] = 2;
+      }
+      for (int i = 0; i < m; ++i) {
+        if (i == k) continue;
+        const double f = A[i * m + k];
+        for (int j = k + 1; j < m; ++j) {
+          double t = f * A[k * m + j];
+          A[i * m + j] = A[i * m + j] - t;
+        }
+        for (int j = 0; j < m; ++j) {
+          if (kind[k * m + j] == 0) continue;
+          double t = f * B[k * m + j];
+          if (kind[i * m + j] == 0) {
+            B[i * m + j] = -t;
+          } else {
+            double bij = kind[i * m + j] == 1 ? 1.0 : B[i * m + j];
+            B[i * m + j] = bij - t;
+          }
+          kind[i * m + j] = 2;
+        }
+      }
+    }
+    for (int e = 0; e < m * m; ++e) Binv[g * m * m + e] = B[e];
+  }
+  return first_singular;
+}
+
+// x = A^{-1} b per block with the inverse from oracle_gj_inverse: each row a
+// left-to-right sum, x_i = RN(...RN(RN(B_i0 b_0) + RN(B_i1 b_1))... + RN(B_i,m-1 b_m-1)).
+// x may alias b.
+void oracle_gj_apply(int64_t G, int m, const double* Binv, const double* b, double* x) {
+  std::vector<double> y(m);
+  for (int64_t g = 0; g < G; ++g) {
+    const double* B = Binv + g * m * m;
+    for (int i = 0; i < m; ++i) {
+      double s = B[i * m] * b[g * m];
+      for (int j = 1; j < m; ++j) {
+        double t = B[i * m + j] * b[g * m + j];
+        s = s + t;
+      }
+      y[i] = s;
+    }
+    for (int i = 0; i < m; ++i) x[g * m + i] = y[i];
+  }
+}
+
 // O7: x = U^{-1} L^{-1} P b per block; x may alias b.  Forward then back
 // substitution in index order, each Σ as sequential RN subtractions.
 void oracle_lu_solve(int64_t G, int m, const double* LU, const int32_t* piv,
@@ -448,7 +526,8 @@ struct OracleSbdfParams {
   double A, B, eps;
   double lam_E, lam_I;
   double h, rtol, atol, tol_nl;
-  int32_t linsol;         // 0: block LU solve (task-local); 1: GMRES, block-LU
+  int32_t linsol;         // 0: block LU solve (task-local); 2: block inverse by
+                          // symbolic Gauss-Jordan; 1: GMRES, block-LU
                           //    preconditioner (the paper's global Newton)
   int32_t maxl;           // GMRES Krylov dimension
   double lin_tol;         // GMRES relative residual tolerance
@@ -540,7 +619,8 @@ int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
     jac_implicit(P, G, z.data(), M.data());
     oracle_scale_add_identity(G, 3, -gamma, M.data());
     if (P->linsol == 1) Mop = M;            // the operator; M becomes its LU
-    int64_t sing = oracle_lu_factor(G, 3, M.data(), piv.data());
+    int64_t sing = P->linsol == 2 ? oracle_gj_inverse(G, 3, M.data(), Mop.data())
+                                  : oracle_lu_factor(G, 3, M.data(), piv.data());
     st->setups++;
     if (sing) { st->singular = sing; st->fails++; return 1; }
     int maxit = (P->newton_mode == 2) ? 50 : P->K;
@@ -554,6 +634,8 @@ int oracle_sbdf_integrate(const OracleSbdfParams* P, double* y, int64_t nsteps,
         double res = 0.0;
         st->lin_iters += oracle_gmres(G, 3, Mop.data(), M.data(), piv.data(), r.data(),
                                       delta.data(), P->maxl, P->lin_tol, &res);
+      } else if (P->linsol == 2) {
+        oracle_gj_apply(G, 3, Mop.data(), r.data(), delta.data());
       } else {
         oracle_lu_solve(G, 3, M.data(), piv.data(), r.data(), delta.data());
       }

@@ -134,3 +134,104 @@ def test_scale_add_identity():
     Ad = synth.dyadic(17, 45).numpy().reshape(5, 3, 3)
     M = oracle.scale_add_identity(-0.5, Ad)
     assert np.array_equal(M, -0.5 * Ad + np.eye(3))                 # dyadic: exact
+
+
+# ---------------------------------------------------------------------------
+# Block inverse by symbolic Gauss-Jordan (the paper's task-local solver,
+# P:389-390): pinned by the adjugate formula in exact rationals, numpy's
+# LAPACK inverse, structural special cases and the exact-arithmetic identity
+# A·A^{-1} = I.
+
+def inv_exact(M):
+    """Exact inverse by the adjugate (cofactor) formula, independent of GJ."""
+    m = len(M)
+    d = det_exact(M)
+    inv = [[F(0)] * m for _ in range(m)]
+    for i in range(m):
+        for j in range(m):
+            minor = [[M[r][c] for c in range(m) if c != i] for r in range(m) if r != j]
+            inv[i][j] = (-1) ** (i + j) * det_exact(minor) / d
+    return inv
+
+
+def test_gj_identity_and_diagonal_exact():
+    D = np.zeros((4, 3, 3))
+    diag = [(1.0, 1.0, 1.0), (2.0, -4.0, 0.5), (3.0, 7.0, 1e-3), (-1.0, 10.0, 5e5)]
+    for g, d in enumerate(diag):
+        D[g] = np.diag(d)
+    B, flag = oracle.gj_inverse(D)
+    assert flag == 0
+    for g, d in enumerate(diag):
+        expect = np.diag([1.0 / x for x in d])          # RN(1/d): one rounding each
+        assert np.array_equal(B[g], expect)
+
+
+def test_gj_small_integer_blocks_vs_exact_rationals():
+    rng = np.random.default_rng(11)
+    checked = 0
+    while checked < 300:
+        M = rng.integers(-4, 5, (3, 3)).astype(float)
+        M += np.diag(rng.integers(5, 9, 3))              # leading minors nonzero
+        Mi = [[int(v) for v in row] for row in M]
+        if det_exact(Mi) == 0 or Mi[0][0] == 0 or det_exact([r[:2] for r in Mi[:2]]) == 0:
+            continue
+        B, flag = oracle.gj_inverse(M[None])
+        assert flag == 0
+        ex = inv_exact(Mi)
+        for i in range(3):
+            for j in range(3):
+                e = float(ex[i][j])
+                # a handful of roundings on well-conditioned blocks
+                assert abs(B[0, i, j] - e) <= 64 * 2 ** -53 * max(1.0, abs(e)), (M, i, j)
+        checked += 1
+
+
+def test_gj_random_blocks_vs_lapack_and_identity():
+    G = 5000
+    u = synth.uniform(synth.S_CELL, 9 * G, -1, 1).numpy().reshape(G, 3, 3)
+    M = u + 4.0 * np.eye(3)[None]                         # diagonally dominant: no pivoting needed
+    B, flag = oracle.gj_inverse(M)
+    assert flag == 0
+    ref = np.linalg.inv(M)
+    assert np.max(np.abs(B - ref) / np.maximum(np.abs(ref), 1e-3)) <= 1e-13
+    I = np.einsum("gij,gjk->gik", M, B)
+    assert np.max(np.abs(I - np.eye(3)[None])) <= 1e-14
+
+
+def test_gj_apply_is_left_to_right_matvec():
+    G = 1000
+    B = synth.uniform(3, 9 * G, -1, 1).numpy().reshape(G, 3, 3)
+    b = synth.uniform(4, 3 * G, -1, 1).numpy()
+    x = oracle.gj_apply(B, b).reshape(G, 3)
+    bb = b.reshape(G, 3)
+    for g in range(0, G, 97):
+        for i in range(3):
+            s = B[g, i, 0] * bb[g, 0]
+            s = s + B[g, i, 1] * bb[g, 1]
+            s = s + B[g, i, 2] * bb[g, 2]
+            assert x[g, i] == s
+
+
+def test_gj_zero_leading_pivot_flags_block():
+    # nonsingular, but Gauss-Jordan without pivoting meets a zero pivot: the
+    # method's documented limitation (the symbolic sequence has no pivoting)
+    M = np.stack([np.eye(3), np.array([[0.0, 1, 0], [1, 0, 0], [0, 0, 1]]), np.eye(3)])
+    _, flag = oracle.gj_inverse(M)
+    assert flag == 2
+
+
+def test_gj_newton_matrix_equals_lu_solution():
+    # On Brusselator Newton matrices M = I - γJ the GJ inverse and the LU
+    # solve give the same correction up to rounding
+    G = 2000
+    u = synth.uniform(synth.S_CELL, G, 0.5, 2.0).numpy()
+    y = np.stack([u, 3.0 * u, 3.5 - 0.1 * u], 1).reshape(-1)
+    J = oracle.bruss_jacobian(y)
+    M = np.eye(3)[None] - 2e-3 / 3 * J
+    B, flag = oracle.gj_inverse(M)
+    LU, piv, f2 = oracle.lu_factor(M)
+    assert flag == 0 and f2 == 0
+    r = synth.uniform(7, 3 * G, -1, 1).numpy()
+    x1 = oracle.gj_apply(B, r)
+    x2 = oracle.lu_solve(LU, piv, r)
+    assert np.max(np.abs(x1 - x2) / np.maximum(np.abs(x2), 1e-300)) <= 1e-12
