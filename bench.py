@@ -278,6 +278,13 @@ def other_configs(S, ctx, torch):
     out["C1_1D_64cells"] = {
         "composed_graph_steps_per_s": round(stepper_rate(c1, 64, 1000, use_graph=True), 1),
         "fused_graph_steps_per_s": round(stepper_rate(c1, 64, 1000, use_graph=True, fused=True), 1)}
+    # the paper's own task-local block solve (symbolic Gauss-Jordan inverse,
+    # P:389-390, DESIGN R29) in the fused step at the bench workload (C5 slab)
+    c5 = S.bruss_params(dim=3, nx=256, ny=256, nz=256)
+    r5 = stepper_rate(c5, 256 ** 3, 100, use_graph=True, fused=True, linsol=2)
+    out["C5_block_inverse_GJ"] = {"fused_steps_per_s": round(r5, 1), "cell_steps_per_s": r5 * 256 ** 3,
+                                  "note": "linsol=2: block inverse by symbolic Gauss-Jordan (ablation; "
+                                          "the headline uses the LU solve)"}
     c3 = S.bruss_params(dim=3, nx=128, ny=128, nz=128)
     r3 = stepper_rate(c3, 128 ** 3, 200, use_graph=True, fused=True)
     out["C3_3D_128cubed"] = {"fused_steps_per_s": round(r3, 1), "cell_steps_per_s": r3 * 128 ** 3}

@@ -44,7 +44,7 @@ int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, do
                  double rtol, double atol, const double* y, const double* fE, const double* hin,
                  double* hout, double* z, double* partials, unsigned long long* d_first,
                  int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end,
-                 const FusedFold* fold);
+                 const FusedFold* fold, bool gj);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
                double* d_min, double* d_nu, int* d_err);
 int fused_finalize_pending(SUNBW_Context ctx, double* pending, int K, int64_t nglobal, double* d_min,
@@ -207,7 +207,7 @@ int enqueue_step(Stepper* S, bool first) {
       {
         Timed t(S, BW_K_FUSED_NEWTON);
         TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
-                                S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr));
+                                S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr, o.linsol == 2));
       }
       if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
       fold.prev_parts = nb;
@@ -215,13 +215,13 @@ int enqueue_step(Stepper* S, bool first) {
         Timed t(S, BW_K_FUSED_NEWTON);
         TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
                                 S->d_partials + (int64_t)nb * (o.K + 1), S->d_first, &nb2, &fa, 0, tpp,
-                                fk));
+                                fk, o.linsol == 2));
       }
     } else {
       Timed t(S, BW_K_FUSED_NEWTON);
       TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y,
                               adv_in_kernel ? nullptr : fE_n, fEp, fE, z, S->d_partials, S->d_first, &nb,
-                              adv_in_kernel ? &fa : nullptr, 0, -1, fk));
+                              adv_in_kernel ? &fa : nullptr, 0, -1, fk, o.linsol == 2));
     }
     if (!fold_in_kernel) {
       Timed t(S, BW_K_WRMS);
@@ -401,8 +401,10 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   *out = nullptr;
   if (opt->K < 1 || opt->K > kMaxK || !(opt->h > 0) || (opt->newton_mode != 0 && opt->newton_mode != 1))
     return SUNBW_ERR_ARG;
-  if (opt->fused && (opt->newton_mode != 0 || opt->K > 8 || opt->linsol != 0)) return SUNBW_ERR_UNSUPPORTED;
-  if (opt->linsol != 0 && (opt->linsol != 1 || opt->maxl < 1 || opt->maxl > 60)) return SUNBW_ERR_ARG;
+  if (opt->linsol < 0 || opt->linsol > 2 || (opt->linsol == 1 && (opt->maxl < 1 || opt->maxl > 60)))
+    return SUNBW_ERR_ARG;
+  if (opt->fused && (opt->newton_mode != 0 || opt->K > 8 || opt->linsol == 1)) return SUNBW_ERR_UNSUPPORTED;
+  if (!opt->fused && opt->linsol == 2) return SUNBW_ERR_UNSUPPORTED;   // block inverse: fused step only
   SUNBW_Context ctx = y0->ctx;
   int64_t G = sunbw::bw_local_cells(prob);
   if (y0->local_len != 3 * G) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);

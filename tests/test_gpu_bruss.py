@@ -428,3 +428,59 @@ def test_fused_newton_iteration_counts(S, ctx, K, shape):
     assert rc == 0 and stats["newton_iters"] == K * steps
     assert_bits_equal(y, yref, f"fused K={K} {shape}")
     assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-12 * stref["last_nu"]
+
+
+# ------------------------------------------- block inverse (symbolic GJ, R29)
+@pytest.mark.parametrize("case", ["C1", "3D", "C4", "extreme", "K1"])
+def test_fused_block_inverse_matches_oracle(S, ctx, case):
+    """The paper's task-local block solve — each 3x3 Newton block inverted by
+    symbolic Gauss-Jordan and applied as a matrix-vector product (P:389-390,
+    linsol = 2) — in the fused step: bit-identical to the oracle's GJ path."""
+    K, h = 3, 1e-3
+    if case == "C1":
+        nx, ny, nz, steps = 64, 1, 1, 1000
+        y0 = oracle.bruss_ic(nx)
+        params, dim = S.bruss_params(dim=1, nx=nx), 1
+        ro = False
+    elif case in ("3D", "K1"):
+        nx, ny, nz, steps = 128, 6, 4, 6
+        y0 = oracle.bruss_ic(nx, ny, nz)
+        params, ro = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz), False
+        K = 1 if case == "K1" else 3
+    else:
+        G, steps = 100_003, 3
+        nx, ny, nz = G, 1, 1
+        u = synth.uniform(synth.S_CELL, G, 0, 1).numpy()
+        y0 = np.stack([1.0 + 0.1 * u, 3.5 + 0.1 * u, 3.0 + 0.1 * u], 1).reshape(-1)
+        if case == "extreme":
+            y0 = _inject_extremes(y0, 79)
+        params, ro = S.bruss_params(dim=1, nx=G, reaction_only=True), True
+    k = kappas(nx, ny, nz) if not ro else (0.0, 0.0, 0.0)
+    rc2, yref, stref, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=K, nx=nx, ny=ny, nz=nz,
+                                                kx=k[0], ky=k[1], kz=k[2], h=h, reaction_only=ro,
+                                                linsol=2)
+    rc, y, stats = run_gpu(S, ctx, params, y0, steps, h=h, K=K, fused=True, linsol=2)
+    if case != "extreme":
+        assert rc2 == 0 and rc == 0
+        assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-12 * stref["last_nu"]
+    assert_bits_equal(y, yref, f"GJ {case}")
+
+
+def test_block_inverse_zero_pivot_is_singular(S, ctx):
+    """Gauss-Jordan without row exchanges meets a zero pivot on a block that
+    partial pivoting would factor: reported as a singular block (the
+    method's limitation), like the oracle."""
+    G = 300
+    u = synth.uniform(synth.S_CELL, G, 0.5, 1.5).numpy()
+    y0 = np.stack([u, 2.0 * u, 3.0 + 0 * u], 1).reshape(-1)
+    # M_00 = 1 - γ(2uv - (w + 1)) = 0 for cell 17: choose v so that 2uv = w + 1 + 1/γ
+    h = 1e-3
+    y0[3 * 17 + 1] = (y0[3 * 17 + 2] + 1.0 + 1.0 / h) / (2.0 * y0[3 * 17])
+    M = np.eye(3)[None] - h * oracle.bruss_jacobian(y0)
+    if M[17, 0, 0] != 0.0:
+        pytest.skip("no exact zero pivot from this construction")
+    _, flag = oracle.gj_inverse(M)
+    assert flag == 18
+    params = S.bruss_params(dim=1, nx=G, reaction_only=True)
+    rc, _, stats = run_gpu(S, ctx, params, y0, 1, h=h, K=3, fused=True, linsol=2)
+    assert rc != 0 and stats["singular"] == 18
