@@ -173,7 +173,7 @@ def run_reference(args, world, rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (paper IC, P:376-382)",
-        "config": {"workload": "C5 slab sample (oracle)", "cells": cells, "K": 3, "h": 1e-3},
+        "config": workload_config(world, "oracle (serial CPU, bounded sample: see cpu_baseline)"),
         "cpu_baseline": {"value": v, "unit": "cell-steps/s", "cores": 1, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": v, "unit": "cell-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,6 +183,15 @@ def run_reference(args, world, rank):
 
 METRIC = ("advection-reaction throughput, cell time-steps/s (3D Brusselator, 256^3 cells/GPU, "
           "SBDF2 + K=3 block-LU Newton, fp64)")
+
+
+def workload_config(world, mode, n_ax=256):
+    """The `config` object of both arms (BASELINE configs[4], one slab per GPU)."""
+    return {"workload": "C5: 3D Brusselator advection-reaction, 256^3 cells per GPU "
+                        "(configs[4]; N=1 is one slab)",
+            "cells_per_gpu": n_ax ** 3, "global_grid": [n_ax, n_ax, n_ax * world],
+            "K": 3, "h": 1e-3, "mode": mode, "parallelism": f"z-slab x{world}",
+            "l2": "inputs larger than L2 (state 403 MB per vector)"}
 
 
 def cpu_baseline_sample(planes=64, steps=15):
@@ -492,11 +501,7 @@ def main():
             "steps_per_s": args.steps / (ms * 1e-3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper's Gaussian IC, P:376-382, on the 3D grid)",
-            "config": {"workload": "C5: 3D Brusselator advection-reaction, 256^3 cells per GPU "
-                                   "(configs[4]; N=1 is one slab)",
-                       "cells_per_gpu": G, "global_grid": [n_ax, n_ax, n_ax * world],
-                       "K": 3, "h": 1e-3, "mode": args.mode, "parallelism": f"z-slab x{world}",
-                       "l2": "inputs larger than L2 (state 403 MB per vector)"},
+            "config": workload_config(world, args.mode, n_ax),
             "roofline": roofline, "step_bytes": step_bytes, "composed_equiv_bytes_per_step": (820 + 388 * 3) * G,
             "step_GB/s": round(step_bytes / (ms / args.steps * 1e-3) / 1e9, 1),
             "kernels": kernels, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
