@@ -1,5 +1,5 @@
 # A/B of fused-step variants: tests on the default build, then the bench per variant
-python -m pytest tests -m gpu -x -q -k "bruss or nccl or multiinstance or ark or numerics" > gpurun_out/t_br.log 2>&1; tail -1 gpurun_out/t_br.log
+timeout 600 python -m pytest tests -m gpu -x -q -k "bruss or nccl or multiinstance or ark or numerics" > gpurun_out/t_br.log 2>&1; tail -1 gpurun_out/t_br.log
 for v in default ${VARIANTS}; do
   if [ $v = default ]; then unset SUNBW_LIB; else export SUNBW_LIB=$PWD/build/$v/libsunbw.so; fi
   timeout 300 python bench.py --no-ops --no-cpu --steps 200 > gpurun_out/ab_$v.json 2>/dev/null
