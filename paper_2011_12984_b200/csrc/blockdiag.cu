@@ -330,6 +330,115 @@ __global__ void __launch_bounds__(tpc<M>()) k_lu_solve_tma(sunbw::pipe::IO<3, 1>
       });
 }
 
+// ---- block inverse by symbolic Gauss-Jordan (the paper's task-local block
+// solve; DESIGN R29).  On
+// [A | I] without row exchanges; the identity block's structure is
+// data-independent, so the "symbolic" skipping of its structural zeros and
+// ones is resolved at compile time: at step k row k holds values in columns
+// j <= k (B_kk was the structural 1, now p = RN(1/a_kk)), and every other
+// row gets column k as -RN(f B_kk) and columns j < k as RN(B_ij - RN(f B_kj)).
+template <int M>
+__device__ __forceinline__ bool gj_regs(double (&a)[M][M], double (&B)[M][M]) {
+  bool sing = false;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    sing |= a[k][k] == 0.0;
+    const double p = __drcp_rn(a[k][k]);              // RN(1/a_kk) (IEEE 1/0 = inf)
+#pragma unroll
+    for (int j = k + 1; j < M; ++j) a[k][j] = __dmul_rn(a[k][j], p);
+#pragma unroll
+    for (int j = 0; j < k; ++j) B[k][j] = __dmul_rn(B[k][j], p);
+    B[k][k] = p;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      if (i == k) continue;
+      const double f = a[i][k];
+#pragma unroll
+      for (int j = k + 1; j < M; ++j) a[i][j] = __dsub_rn(a[i][j], __dmul_rn(f, a[k][j]));
+#pragma unroll
+      for (int j = 0; j < k; ++j) B[i][j] = __dsub_rn(B[i][j], __dmul_rn(f, B[k][j]));
+      B[i][k] = -__dmul_rn(f, B[k][k]);
+    }
+  }
+  return sing;
+}
+
+template <int M>
+__global__ void __launch_bounds__(tpc<M>()) k_gj_inverse_tma(sunbw::pipe::IO<1, 1> io, int64_t G,
+                                                            unsigned long long* first_singular) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  sunbw::pipe::run<tpc<M>(), kStagesLU>(
+      io, G, smem, [&](int, int64_t g, const unsigned char** ip, unsigned char** op) {
+        const double* ain = reinterpret_cast<const double*>(ip[0]);
+        double a[M][M], B[M][M];
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+          for (int j = 0; j < M; ++j) a[i][j] = ain[i * M + j];
+        const bool sing = gj_regs<M>(a, B);
+        double* bout = reinterpret_cast<double*>(op[0]);
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+          for (int j = 0; j < M; ++j) bout[i * M + j] = B[i][j];
+        if (sing) atomicMin(first_singular, (unsigned long long)(g + 1));
+      });
+}
+
+// plain one-thread-per-block variants (operands not 16-B aligned)
+template <int M>
+__global__ void k_gj_inverse(double* A, int64_t G, unsigned long long* first_singular) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    double a[M][M], B[M][M];
+#pragma unroll
+    for (int e = 0; e < M * M; ++e) a[e / M][e % M] = A[g * M * M + e];
+    if (gj_regs<M>(a, B)) atomicMin(first_singular, (unsigned long long)(g + 1));
+#pragma unroll
+    for (int e = 0; e < M * M; ++e) A[g * M * M + e] = B[e / M][e % M];
+  }
+}
+template <int M>
+__global__ void k_gj_apply(const double* B, const double* b, double* x, int64_t G) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    double r[M], y[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) r[i] = b[g * M + i];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      double s = __dmul_rn(B[g * M * M + i * M], r[0]);
+#pragma unroll
+      for (int j = 1; j < M; ++j) s = __dadd_rn(s, __dmul_rn(B[g * M * M + i * M + j], r[j]));
+      y[i] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) x[g * M + i] = y[i];
+  }
+}
+
+// x = A^{-1} b: each row a left-to-right sum (R29); x may alias b
+template <int M>
+__global__ void __launch_bounds__(tpc<M>()) k_gj_apply_tma(sunbw::pipe::IO<2, 1> io, int64_t G) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  sunbw::pipe::run<tpc<M>(), kStagesLU>(
+      io, G, smem, [&](int, int64_t, const unsigned char** ip, unsigned char** op) {
+        const double* B = reinterpret_cast<const double*>(ip[0]);
+        const double* b = reinterpret_cast<const double*>(ip[1]);
+        double r[M], x[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) r[i] = b[i];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          double s = __dmul_rn(B[i * M], r[0]);
+#pragma unroll
+          for (int j = 1; j < M; ++j) s = __dadd_rn(s, __dmul_rn(B[i * M + j], r[j]));
+          x[i] = s;
+        }
+        double* xo = reinterpret_cast<double*>(op[0]);
+#pragma unroll
+        for (int i = 0; i < M; ++i) xo[i] = x[i];
+      });
+}
+
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 // persistent grid: resident CTAs per SM from the shared-memory footprint
@@ -382,6 +491,45 @@ int launch_lu_solve(SUNBW_Context ctx, int64_t G, const double* LU, const int32_
   return ctx_check_launch(ctx);
 }
 
+constexpr int kOccGJ = 16;
+
+template <int M>
+int launch_gj_inverse(SUNBW_Context ctx, int64_t G, double* A, unsigned long long* d_first) {
+  constexpr int T = tpc<M>();
+  if (!aligned16(A)) {
+    k_gj_inverse<M><<<grid_for(ctx, G, 128, kOccGJ), 128, 0, ctx->stream>>>(A, G, d_first);
+    ctx->launches++;
+    return ctx_check_launch(ctx);
+  }
+  sunbw::pipe::IO<1, 1> io{{(const unsigned char*)A}, {M * M * 8}, {(unsigned char*)A}, {M * M * 8}};
+  const int smem = 128 + T * (kStagesLU * M * M * 8 + M * M * 8);
+  static bool attr = cudaFuncSetAttribute(k_gj_inverse_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          smem) == cudaSuccess;
+  if (!attr) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  k_gj_inverse_tma<M><<<grid_tma(ctx, G, T, smem), T, smem, ctx->stream>>>(io, G, d_first);
+  ctx->launches++;
+  return ctx_check_launch(ctx);
+}
+
+template <int M>
+int launch_gj_apply(SUNBW_Context ctx, int64_t G, const double* B, const double* b, double* x) {
+  constexpr int T = tpc<M>();
+  if (!(aligned16(B) && aligned16(b) && aligned16(x))) {
+    k_gj_apply<M><<<grid_for(ctx, G, 128, kOccGJ), 128, 0, ctx->stream>>>(B, b, x, G);
+    ctx->launches++;
+    return ctx_check_launch(ctx);
+  }
+  sunbw::pipe::IO<2, 1> io{{(const unsigned char*)B, (const unsigned char*)b}, {M * M * 8, M * 8},
+                           {(unsigned char*)x}, {M * 8}};
+  const int smem = 128 + T * (kStagesLU * (M * M * 8 + M * 8) + M * 8);
+  static bool attr = cudaFuncSetAttribute(k_gj_apply_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          smem) == cudaSuccess;
+  if (!attr) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  k_gj_apply_tma<M><<<grid_tma(ctx, G, T, smem), T, smem, ctx->stream>>>(io, G);
+  ctx->launches++;
+  return ctx_check_launch(ctx);
+}
+
 }  // namespace
 
 // ============================================================ internal API
@@ -420,6 +568,25 @@ int lu_solve(SUNBW_Context ctx, int64_t G, int m, const double* LU, const int32_
   case M: return launch_lu_solve<M>(ctx, G, LU, piv, b, x);
   DISPATCH_M(m, LUS)
 #undef LUS
+}
+
+// block inverses in place (symbolic Gauss-Jordan, R29); d_first as lu_factor
+int gj_inverse(SUNBW_Context ctx, int64_t G, int m, double* A, unsigned long long* d_first, bool reset) {
+  if (reset && cudaMemsetAsync(d_first, 0xFF, sizeof(unsigned long long), ctx->stream) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  if (G <= 0) return 0;
+#define GJI(M) \
+  case M: return launch_gj_inverse<M>(ctx, G, A, d_first);
+  DISPATCH_M(m, GJI)
+#undef GJI
+}
+
+int gj_apply(SUNBW_Context ctx, int64_t G, int m, const double* B, const double* b, double* x) {
+  if (G <= 0) return 0;
+#define GJA(M) \
+  case M: return launch_gj_apply<M>(ctx, G, B, b, x);
+  DISPATCH_M(m, GJA)
+#undef GJA
 }
 
 int block_matvec(SUNBW_Context ctx, int64_t G, int m, const double* A, const double* x, double* y) {
@@ -514,13 +681,24 @@ extern "C" SUNLinearSolver SUNLinSol_B200BatchedLU(N_Vector y, SUNMatrix A) {
   return S;
 }
 
+// The paper's task-local block solve (DESIGN R29): Setup replaces
+// every block by its inverse (symbolic Gauss-Jordan, no row exchanges; a
+// zero pivot flags the block), Solve applies it.  Same handle type and
+// Setup/Solve/LastFlag/Free calls as the batched LU.
+extern "C" SUNLinearSolver SUNLinSol_B200BatchedGJ(N_Vector y, SUNMatrix A) {
+  SUNLinearSolver S = SUNLinSol_B200BatchedLU(y, A);
+  if (S) S->type = 2;
+  return S;
+}
+
 extern "C" int SUNLinSolSetup(SUNLinearSolver S0, SUNMatrix A) {
   if (S0 && S0->type == 1) return sunbw::spgmr_setup(S0, A);
   auto* S = (LinSolImpl*)S0;
   if (!S || !A) return SUNBW_ERR_ARG;
   if (A->ctx != S->ctx) return ctx_set_err(S->ctx, SUNBW_ERR_CONTEXT);
   if (A->nblocks != S->nblocks || A->m != S->m) return ctx_set_err(S->ctx, SUNBW_ERR_LENGTH);
-  int e = sunbw::lu_factor(S->ctx, S->nblocks, S->m, A->d, S->d_piv, S->d_first);
+  int e = S->type == 2 ? sunbw::gj_inverse(S->ctx, S->nblocks, S->m, A->d, S->d_first)
+                       : sunbw::lu_factor(S->ctx, S->nblocks, S->m, A->d, S->d_piv, S->d_first);
   if (e) return e;
   S->flag_pending = true;
   if (S->deferred) return 0;
@@ -535,6 +713,7 @@ extern "C" int SUNLinSolSolve(SUNLinearSolver S, SUNMatrix A, N_Vector x, N_Vect
   if (x->ctx != S->ctx || b->ctx != S->ctx || A->ctx != S->ctx) return ctx_set_err(S->ctx, SUNBW_ERR_CONTEXT);
   if (x->local_len != S->nblocks * S->m || b->local_len != x->local_len)
     return ctx_set_err(S->ctx, SUNBW_ERR_LENGTH);
+  if (S->type == 2) return sunbw::gj_apply(S->ctx, S->nblocks, S->m, A->d, b->d, x->d);
   return sunbw::lu_solve(S->ctx, S->nblocks, S->m, A->d, S->d_piv, b->d, x->d);
 }
 

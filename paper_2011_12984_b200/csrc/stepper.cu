@@ -259,6 +259,8 @@ int enqueue_step(Stepper* S, bool first) {
     Timed t(S, BW_K_LU_SETUP);
     if (S->gm)   // global Newton: M stays the GMRES operator, its LU preconditions
       TRY(sunbw::spgmr_setup_raw(S->gm, S->M, S->d_first));
+    else if (o.linsol == 2)   // the paper's block inverse (R29)
+      TRY(sunbw::gj_inverse(ctx, G, 3, S->M, S->d_first, false));
     else
       TRY(sunbw::lu_factor_noreset(ctx, G, 3, S->M, S->piv, S->d_first));
   }
@@ -289,6 +291,8 @@ int enqueue_step(Stepper* S, bool first) {
         int steps = sunbw::spgmr_solve_raw(S->gm, S->M, S->delta, S->r, o.lin_tol);
         TRY(steps);
         S->st.lin_iters += steps;
+      } else if (o.linsol == 2) {
+        TRY(sunbw::gj_apply(ctx, G, 3, S->M, S->r, S->delta));
       } else {
         TRY(sunbw::lu_solve(ctx, G, 3, S->M, S->piv, S->r, S->delta));
       }
@@ -404,7 +408,6 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   if (opt->linsol < 0 || opt->linsol > 2 || (opt->linsol == 1 && (opt->maxl < 1 || opt->maxl > 60)))
     return SUNBW_ERR_ARG;
   if (opt->fused && (opt->newton_mode != 0 || opt->K > 8 || opt->linsol == 1)) return SUNBW_ERR_UNSUPPORTED;
-  if (!opt->fused && opt->linsol == 2) return SUNBW_ERR_UNSUPPORTED;   // block inverse: fused step only
   SUNBW_Context ctx = y0->ctx;
   int64_t G = sunbw::bw_local_cells(prob);
   if (y0->local_len != 3 * G) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);

@@ -77,7 +77,7 @@ struct _SUNMatrix {
 };
 
 struct _SUNLinearSolver {
-  int type = 0;                 // 0: batched block LU, 1: SPGMR (gmres.cu)
+  int type = 0;                 // 0: batched block LU, 1: SPGMR (gmres.cu), 2: batched GJ inverse
   SUNBW_Context ctx;
   int64_t nblocks;
   int m;
@@ -136,6 +136,10 @@ int block_matvec(SUNBW_Context, int64_t G, int m, const double* A,
 
 int lu_factor_noreset(SUNBW_Context, int64_t G, int m, double* A, int32_t* piv,
                       unsigned long long* d_first);
+// block inverses in place by symbolic Gauss-Jordan (R29) and their apply;
+// reset = false accumulates the first singular block into d_first
+int gj_inverse(SUNBW_Context, int64_t G, int m, double* A, unsigned long long* d_first, bool reset = true);
+int gj_apply(SUNBW_Context, int64_t G, int m, const double* Ainv, const double* b, double* x);
 
 // SPGMR (gmres.cu): dispatched from the SUNLinSol* entry points
 SUNLinearSolver spgmr_create(SUNBW_Context ctx, int64_t G, int m, int maxl, bool block_prec);

@@ -129,6 +129,7 @@ _SIGS = {
     "SUNMatMatvec": (_I, [_P, _P, _P]),
     "SUNMatDestroy": (None, [_P]),
     "SUNLinSol_B200BatchedLU": (_P, [_P, _P]),
+    "SUNLinSol_B200BatchedGJ": (_P, [_P, _P]),
     "SUNLinSolSetup": (_I, [_P, _P]),
     "SUNLinSolSolve": (_I, [_P, _P, _P, _P, _D]),
     "SUNLinSolLastFlag": (_I64, [_P]),
@@ -423,12 +424,16 @@ def SUNMatMatvec(A: SUNMatrix, x: NVector, y: NVector) -> int:
 
 
 class SUNLinearSolver:
-    """Batched block LU (default) or, with spgmr_maxl, SPGMR (GMRES with the
+    """Batched block LU (default); with gj=True the paper's block inverse by
+    symbolic Gauss-Jordan; with spgmr_maxl, SPGMR (GMRES with the
     block LU as optional preconditioner)."""
 
-    def __init__(self, y: NVector, A: SUNMatrix, spgmr_maxl: int = 0, block_prec: bool = True):
+    def __init__(self, y: NVector, A: SUNMatrix, spgmr_maxl: int = 0, block_prec: bool = True,
+                 gj: bool = False):
         if spgmr_maxl:
             h = lib().SUNLinSol_B200SPGMR(y, A, spgmr_maxl, int(block_prec))
+        elif gj:
+            h = lib().SUNLinSol_B200BatchedGJ(y, A)
         else:
             h = lib().SUNLinSol_B200BatchedLU(y, A)
         if not h:

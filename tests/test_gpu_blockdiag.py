@@ -149,3 +149,67 @@ def test_newton_matrix_from_jacobian(S, ctx):
     LU, piv, _ = oracle.lu_factor(Mref)
     assert_bits_equal(Jd.reshape(-1), LU.reshape(-1), "LU(M)")
     P.destroy()
+
+
+# ------------------------------------------- block inverse (symbolic GJ, R29)
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("G", [1, 129, 70001])
+@pytest.mark.parametrize("aligned", [True, False])
+def test_gj_inverse_apply_bit_exact(S, ctx, m, G, aligned):
+    """SUNLinSol_B200BatchedGJ: Setup replaces every block by its inverse
+    (symbolic Gauss-Jordan), Solve applies it; bit-identical to
+    the oracle (TMA-staged and plain kernels)."""
+    A = blocks(60 + m, G, m, diag=2.0)                  # no zero pivots
+    off = 0 if aligned else 1
+    buf = torch.empty(G * m * m + off, dtype=torch.float64, device="cuda")
+    Ad = buf[off:].view(G, m, m)
+    Ad.copy_(A)
+    M = S.SUNMatrix(ctx, Ad)
+    bbuf = torch.empty(G * m + off, dtype=torch.float64, device="cuda")
+    b = bbuf[off:]
+    b.copy_(synth.uniform(70, G * m, -1, 1))
+    x = torch.empty_like(b)
+    vb, vx = S.NVector(ctx, b), S.NVector(ctx, x)
+    LS = S.SUNLinearSolver(vb, M, gj=True)
+    assert S.SUNLinSolSetup(LS, M) == 0 and S.SUNLinSolLastFlag(LS) == 0
+    Binv, flag = oracle.gj_inverse(A.numpy())
+    assert flag == 0
+    assert_bits_equal(Ad.reshape(-1), Binv.reshape(-1), f"GJ inverse m={m} G={G}")
+    S.SUNLinSolSolve(LS, M, vx, vb)
+    ctx.check("gj apply")
+    assert_bits_equal(x, oracle.gj_apply(Binv, b.cpu().numpy()), f"GJ apply m={m} G={G}")
+
+
+def test_gj_zero_pivot_flag(S, ctx):
+    G = 1000
+    A = blocks(80, G, 3, diag=2.0)
+    A[437] = torch.tensor([[0.0, 1.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.0, 1.0]], dtype=torch.float64)
+    A[900, 0, 0] = 0.0
+    Ad = A.cuda().contiguous()
+    M = S.SUNMatrix(ctx, Ad)
+    b = torch.zeros(3 * G, dtype=torch.float64, device="cuda")
+    LS = S.SUNLinearSolver(S.NVector(ctx, b), M, gj=True)
+    assert S.SUNLinSolSetup(LS, M) > 0                   # recoverable
+    assert S.SUNLinSolLastFlag(LS) == 438
+    assert oracle.gj_inverse(A.numpy())[1] == 438
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_stepper_block_inverse_composed_and_fused(S, ctx, fused):
+    """C1 to t = 1 with the paper's block solve (linsol = 2) through the
+    composed N_Vector/solver kernels and through the fused step: both
+    bit-identical to the oracle's GJ path."""
+    nx, steps = 64, 1000
+    y0 = oracle.bruss_ic(nx)
+    rc2, yref, stref, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=nx, kx=0.01 * nx, h=1e-3,
+                                                linsol=2)
+    P = S.Problem(ctx, S.bruss_params(dim=1, nx=nx))
+    yd = torch.from_numpy(y0).cuda()
+    yout = torch.empty_like(yd)
+    st = S.Stepper(P, S.NVector(ctx, yd), S.stepper_options(h=1e-3, K=3, fused=fused, linsol=2))
+    rc, stats = st.advance(steps, S.NVector(ctx, yout))
+    st.destroy()
+    P.destroy()
+    assert rc == 0 and rc2 == 0
+    assert_bits_equal(yout, yref, f"C1 GJ fused={fused}")
+    assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-12 * stref["last_nu"]
