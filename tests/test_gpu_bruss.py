@@ -271,8 +271,9 @@ def run_ranks(S, nranks, fn):
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
-@pytest.mark.parametrize("dim,fused", [(1, False), (3, False), (3, True), ("3big", True)])
-def test_multirank_driver_invariance(S, nranks, dim, fused):
+@pytest.mark.parametrize("dim,fused,linsol", [(1, False, 0), (3, False, 0), (3, True, 0), ("3big", True, 0),
+                                              ("3big", True, 2), (3, False, 2)])
+def test_multirank_driver_invariance(S, nranks, dim, fused, linsol):
     if dim == 1:
         shape = (96, 1, 1)
     elif dim == "3big":
@@ -285,7 +286,7 @@ def test_multirank_driver_invariance(S, nranks, dim, fused):
     params = S.bruss_params(dim=dim, nx=nx, ny=ny, nz=nz)
     k = kappas(nx, ny, nz)
     _, yref, stref, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=nx, ny=ny, nz=nz,
-                                              kx=k[0], ky=k[1], kz=k[2], h=1e-3)
+                                              kx=k[0], ky=k[1], kz=k[2], h=1e-3, linsol=linsol)
 
     def fn(c, r):
         P = S.Problem(c, params)
@@ -294,7 +295,7 @@ def test_multirank_driver_invariance(S, nranks, dim, fused):
         y = torch.from_numpy(y0[off:off + n].copy()).cuda()
         yout = torch.empty_like(y)
         st = S.Stepper(P, S.NVector(c, y), S.stepper_options(h=1e-3, K=3, use_graph=False,
-                                                              fused=fused))
+                                                              fused=fused, linsol=linsol))
         rc, stats = st.advance(steps, S.NVector(c, yout))
         c.stream.synchronize()
         res = (rc, off, yout.cpu().numpy(), stats)
