@@ -297,6 +297,19 @@ def other_configs(S, ctx, torch):
     c3 = S.bruss_params(dim=3, nx=128, ny=128, nz=128)
     r3 = stepper_rate(c3, 128 ** 3, 200, use_graph=True, fused=True)
     out["C3_3D_128cubed"] = {"fused_steps_per_s": round(r3, 1), "cell_steps_per_s": r3 * 128 ** 3}
+    # the paper's integrator (adaptive IMEX ARK3(2)4L[2]SA, f2; composed
+    # kernels, host step-size decisions) on C3 to t = 0.01
+    P = S.Problem(ctx, c3)
+    y3 = torch.empty(3 * 128 ** 3, dtype=torch.float64, device="cuda")
+    S.BW_InitialCondition(P, S.NVector(ctx, y3))
+    A = S.Ark(P, S.NVector(ctx, y3), h0=1e-4, max_steps=2000)
+    ms = timed(lambda: A.evolve(0.01))
+    _, ast = A.evolve(0.01)                      # already at t_end: stats of the run
+    A.destroy(); P.destroy()
+    out["C3_adaptive_ARK"] = {"t_end": 0.01, "accepted_steps": ast["accepted"],
+                              "rejected_steps": ast["rejected_err"] + ast["rejected_nl"],
+                              "newton_iters": ast["newton_iters"], "ms": round(ms, 2),
+                              "steps_per_s": round(ast["accepted"] / (ms * 1e-3), 1)}
     G4 = 10_000_000
     c4 = S.bruss_params(dim=1, nx=G4, reaction_only=True)
     r4 = stepper_rate(c4, G4, 100, use_graph=True, fused=True)
