@@ -255,7 +255,9 @@ def other_configs(S, ctx, torch):
     """The other BASELINE.json configs, measured briefly on this GPU (fixed
     K = 3, h = 1e-3, device-timed with CUDA events):
       C1: 1D Brusselator, 64 cells, t in [0, 1] (1000 steps) — launch-bound:
-          composed step replayed from CUDA graphs, and the fused kernel;
+          composed step replayed from CUDA graphs, the fused step one launch
+          per step (graph replay), and the fused multi-step kernel (the whole
+          Advance in one launch);
       C3: 3D, 128^3 cells, fused single-kernel step (graph replay);
       C4: 1e7 independent reaction cells (batched block Newton only): fused
           steps, and one composed Newton iteration (f_I, residual LC, block
@@ -286,7 +288,10 @@ def other_configs(S, ctx, torch):
     c1 = S.bruss_params(dim=1, nx=64)
     out["C1_1D_64cells"] = {
         "composed_graph_steps_per_s": round(stepper_rate(c1, 64, 1000, use_graph=True), 1),
-        "fused_graph_steps_per_s": round(stepper_rate(c1, 64, 1000, use_graph=True, fused=True), 1)}
+        "fused_steps_per_s": round(stepper_rate(c1, 64, 1000, use_graph=True, fused=True), 1),
+        "fused_one_launch_per_step_graph_steps_per_s": round(
+            stepper_rate(c1, 64, 1000, use_graph=True, fused=True, single_step_launches=True), 1),
+        "note": "fused: the whole Advance in one launch with the state on chip (<= 512 cells)"}
     # the paper's own task-local block solve (symbolic Gauss-Jordan inverse,
     # P:389-390, DESIGN R29) in the fused step at the bench workload (C5 slab)
     c5 = S.bruss_params(dim=3, nx=256, ny=256, nz=256)

@@ -440,6 +440,21 @@ int bw_advection_stencil(void* prob, const double* y, double* f) {
 int64_t bw_local_cells(void* prob) { return ((Prob*)prob)->G; }
 BW_BrussParams bw_params(void* prob) { return ((Prob*)prob)->p; }
 
+bool bw_small_geometry(void* prob, SmallGeom* g) {
+  auto* P = (Prob*)prob;
+  const BW_BrussParams& p = P->p;
+  if (ctx_nranks(P->ctx) != 1 || P->G < 1 || P->G > kSmallCells) return false;
+  g->nx = (int)P->nxl;
+  g->ny = (int)P->nyl;
+  g->nz = (int)P->nzl;
+  g->kx = P->kx;
+  g->ky = P->ky;
+  g->kz = P->kz;
+  g->expl = p.reaction_only ? 2 : (p.kind == 1 ? 1 : 0);
+  g->lam_E = p.lam_E;
+  return true;
+}
+
 bool bw_fused_advection(void* prob, const double* y, FusedAdvection* fa) {
   auto* P = (Prob*)prob;
   const BW_BrussParams& p = P->p;

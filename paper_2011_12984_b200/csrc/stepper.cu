@@ -77,6 +77,9 @@ struct Stepper {
   cudaEvent_t evA = nullptr, evB = nullptr;
   double* d_pending = nullptr;   // K + 2: local [min, sums], flag
   bool deferred = false;
+  // fused fixed-K step of a one-CTA problem: many steps per launch
+  bool small = false;
+  sunbw::SmallGeom sg{};
   int64_t step = 0;
   double t = 0.0;
   BW_StepperStats st{};
@@ -438,6 +441,8 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
     S->gm = sunbw::spgmr_create(ctx, G, 3, opt->maxl, true);
     if (!S->gm) e = SUNBW_ERR_MEM;
   }
+  if (!e && opt->fused && opt->newton_mode == 0 && !opt->single_step_launches)
+    S->small = sunbw::bw_small_geometry(prob, &S->sg);
   if (!e && opt->fused && ctx_nranks(ctx) > 1) {
     S->deferred = opt->newton_mode == 0;
     if (cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -476,7 +481,24 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
   if (S->deferred &&
       cudaMemsetAsync(S->d_pending + S->opt.K + 1, 0, sizeof(double), ctx->stream) != cudaSuccess)
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-  for (int64_t s = 0; s < nsteps; ++s) {
+  if (S->small && nsteps > 0) {
+    // the whole Advance in one launch (state on chip); bit-identical to the
+    // per-step kernels
+    {
+      Timed t(S, BW_K_FUSED_NEWTON);
+      TRY(sunbw::fused_multistep(ctx, S->prob, S->sg, S->G, S->step == 0, nsteps, S->opt.K, S->opt.linsol == 2,
+                                 S->opt.h, S->opt.rtol, S->opt.atol, S->y[S->iy], S->fE[S->ifep], S->y[S->iz],
+                                 S->fE[S->ife], S->d_scal, S->d_err, S->d_first, S->nglobal));
+    }
+    rotate(S);
+    S->step += nsteps;
+    S->t += (double)nsteps * S->opt.h;
+    S->st.steps += nsteps;
+    S->st.setups += nsteps;
+    S->st.newton_iters += nsteps * S->opt.K;
+  }
+  const int64_t nloop = S->small ? 0 : nsteps;  // per-step launches
+  for (int64_t s = 0; s < nloop; ++s) {
     bool first = S->step == 0;
     if (S->opt.use_graph && !first) {
       int key = graph_key(S);

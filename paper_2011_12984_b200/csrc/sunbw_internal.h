@@ -166,6 +166,22 @@ bool bw_fused_advection(void* prob, const double* y, FusedAdvection* fa);
 // step's final launch (self-resetting arrival counter) folds every partial
 // of the step in fixed order and writes either the finalised values (d_min,
 // d_nu, d_err; no communicator) or the local pending record (pending != 0).
+// Geometry of a problem small enough for one CTA (one rank): the fused
+// multi-step kernel keeps the whole state on chip and runs many steps per
+// launch (launch-bound small problems).
+constexpr int kSmallCells = 512;
+struct SmallGeom {
+  int nx, ny, nz;            // global = local extents (one rank)
+  double kx, ky, kz;         // upwind coefficients (terms of extent-1 axes vanish)
+  int expl;                  // 0: upwind advection, 1: f_E = λ_E y, 2: f_E = 0
+  double lam_E;
+};
+bool bw_small_geometry(void* prob, SmallGeom* g);
+int fused_multistep(SUNBW_Context ctx, void* prob, const SmallGeom& gm, int64_t G, bool first, int64_t nsteps,
+                    int K, bool gj, double h, double rtol, double atol, const double* y, const double* hin,
+                    double* y_out, double* hout, double* d_scal, int* d_err, unsigned long long* d_first,
+                    int64_t nglobal);
+
 struct FusedFold {
   int prev_parts;            // partial rows written by earlier launches of this step
   unsigned* counter;         // zero-initialised

@@ -485,3 +485,55 @@ def test_block_inverse_zero_pivot_is_singular(S, ctx):
     params = S.bruss_params(dim=1, nx=G, reaction_only=True)
     rc, _, stats = run_gpu(S, ctx, params, y0, 1, h=h, K=3, fused=True, linsol=2)
     assert rc != 0 and stats["singular"] == 18
+
+
+# ------------------------------------ small problems: many steps per launch
+@pytest.mark.parametrize("case", ["C1", "3D_8cubed", "linear", "reaction_only", "C1_GJ", "K5"])
+def test_fused_multistep_small_problems(S, ctx, case):
+    """A fused fixed-K Advance on one rank with at most 512 cells runs in one
+    launch with the state on chip (launch-bound small problems, P:236-237);
+    it is bit-identical to the oracle and to one launch per step."""
+    K, linsol, kw, steps = 3, 0, {}, 300
+    if case in ("C1", "C1_GJ", "K5"):
+        nx, ny, nz, dim = 64, 1, 1, 1
+        y0 = oracle.bruss_ic(nx)
+        linsol = 2 if case == "C1_GJ" else 0
+        K = 5 if case == "K5" else 3
+        params = S.bruss_params(dim=1, nx=nx)
+        okw = dict(kind=0, nx=nx, kx=kappas(nx)[0])
+    elif case == "3D_8cubed":
+        nx = ny = nz = 8
+        y0 = oracle.bruss_ic(nx, ny, nz)
+        params = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz)
+        k = kappas(nx, ny, nz)
+        okw = dict(kind=0, nx=nx, ny=ny, nz=nz, kx=k[0], ky=k[1], kz=k[2])
+    elif case == "linear":
+        G = 200
+        y0 = synth.uniform(1, 3 * G, 0.5, 1.5).numpy()
+        params = S.bruss_params(dim=1, nx=G, kind=1, lam_E=-1.0, lam_I=-10.0)
+        okw = dict(kind=1, nx=G, lam_E=-1.0, lam_I=-10.0)
+    else:
+        G = 500
+        u = synth.uniform(synth.S_CELL, G, 0, 1).numpy()
+        y0 = np.stack([1.0 + 0.1 * u, 3.5 + 0.1 * u, 3.0 + 0.1 * u], 1).reshape(-1)
+        params = S.bruss_params(dim=1, nx=G, reaction_only=True)
+        okw = dict(kind=0, nx=G, reaction_only=True)
+    rc2, yref, stref, _ = oracle.sbdf_integrate(y0, steps, K=K, h=1e-3, linsol=linsol, **okw)
+    assert rc2 == 0
+    outs = []
+    for single in (False, True):
+        P = S.Problem(ctx, params)
+        yd = torch.from_numpy(y0).cuda()
+        yout = torch.empty_like(yd)
+        st = S.Stepper(P, S.NVector(ctx, yd), S.stepper_options(h=1e-3, K=K, fused=True, linsol=linsol,
+                                                                 single_step_launches=single))
+        l0 = ctx.launches
+        rc, stats = st.advance(100)                    # two calls: the state carries over
+        rc2b, stats = st.advance(steps - 100, S.NVector(ctx, yout))
+        launches = ctx.launches - l0
+        st.destroy(); P.destroy()
+        assert rc == 0 and rc2b == 0 and stats["steps"] == steps and stats["newton_iters"] == K * steps
+        assert_bits_equal(yout.cpu().numpy(), yref, f"{case} single={single}")
+        assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-12 * stref["last_nu"]
+        outs.append(launches)
+    assert outs[0] < outs[1]                           # far fewer launches in one-launch mode
