@@ -9,9 +9,10 @@ generator, which holds none of the method's arithmetic).
 The arithmetic lives in ``oracle.cpp`` (plain C++17, single thread, compiled
 with ``-ffp-contract=off -fno-fast-math``); this module is ctypes marshalling
 over numpy arrays.  Each function cites the passage it follows in
-``oracle.cpp``.  Parity status per function is in DESIGN.md §3; the only
-unpinned item is the full nonlinear Brusselator trajectory ("parity
-unpinned" beyond its piecewise pins, see ``oracle_sbdf_integrate``).
+``oracle.cpp``.  Parity status per function is in DESIGN.md §4; every
+function is pinned — the nonlinear Brusselator trajectory, for which the
+paper prints no values, against an independent Radau IIA integration of
+the semi-discrete equations (tests/test_oracle_bruss.py).
 """
 from __future__ import annotations
 

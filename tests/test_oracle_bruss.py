@@ -245,3 +245,55 @@ def test_sbdf_block_inverse_solver_matches_lu():
     a = oracle.sbdf_integrate(y0, 1, linsol=0, **one)[1]
     b = oracle.sbdf_integrate(y0, 1, linsol=2, **one)[1]
     assert not np.array_equal(a, b) and np.max(np.abs(a - b) / np.abs(a)) <= 1e-15
+
+
+def test_bruss_trajectory_vs_independent_radau():
+    """Pins the nonlinear Brusselator trajectory of the SBDF oracle to an
+    independent integrator: the semi-discrete system of P:369-371 (first-order
+    upwind, periodic, written out here in numpy from the paper's equations,
+    not the oracle's RHS) integrated by scipy's Radau IIA at tight
+    tolerances.  The oracle's SBDF2 solution at t = 0.2 must approach it at
+    second order under h-halving (error ratio ~ 4), with the error of the
+    h = 1e-3 run (C1's step) below 1e-5."""
+    from scipy.integrate import solve_ivp
+
+    nx, b = 32, 1.0
+    c, A, B, eps, alpha = PR["c"], PR["A"], PR["B"], PR["eps"], PR["alpha"]
+    dx = b / nx
+    x = np.arange(nx) * dx
+    p = alpha * np.exp(-((x - b / 2) ** 2) / (2 * (b / 4) ** 2))
+    y0 = np.stack([A + p, B / A + p, 3.0 + p], 1).reshape(-1)
+    assert np.max(np.abs(y0 - oracle.bruss_ic(nx))) <= 1e-15
+
+    def rhs(t, yy):
+        q = yy.reshape(nx, 3)
+        u, v, w = q[:, 0], q[:, 1], q[:, 2]
+        adv = -c * (q - np.roll(q, 1, axis=0)) / dx           # upwind, c > 0, periodic
+        react = np.stack([A - (w + 1) * u + v * u * u, w * u - v * u * u, (B - w) / eps - w * u], 1)
+        return (adv + react).reshape(-1)
+
+    def jac(t, yy):
+        q = yy.reshape(nx, 3)
+        J = np.zeros((3 * nx, 3 * nx))
+        for i in range(nx):
+            u, v, w = q[i]
+            blk = np.array([[2 * u * v - (w + 1), u * u, -u], [w - 2 * u * v, -u * u, u], [-w, 0.0, -1 / eps - u]])
+            J[3 * i:3 * i + 3, 3 * i:3 * i + 3] = blk - c / dx * np.eye(3)
+            im = (i - 1) % nx
+            J[3 * i:3 * i + 3, 3 * im:3 * im + 3] += c / dx * np.eye(3)
+        return J
+
+    T = 0.2
+    ref = solve_ivp(rhs, (0.0, T), y0, method="Radau", jac=jac, rtol=1e-12, atol=1e-13).y[:, -1]
+    errs = []
+    for nsteps in (200, 400, 800):
+        rc, y, _, _ = oracle.sbdf_integrate(y0, nsteps, kind=0, nx=nx, kx=c / dx, h=T / nsteps,
+                                            newton_mode=2, A=A, B=B, eps=eps)
+        assert rc == 0
+        errs.append(np.max(np.abs(y - ref) / np.maximum(np.abs(ref), 1.0)))
+    assert errs[0] <= 1e-5, errs
+    assert 1.7 < math.log2(errs[0] / errs[1]) < 2.3 and 1.7 < math.log2(errs[1] / errs[2]) < 2.3, errs
+    # the fixed K = 3 modified Newton of the parity runs and the bench lands on
+    # the same solution
+    rc, y3, _, _ = oracle.sbdf_integrate(y0, 200, kind=0, nx=nx, kx=c / dx, h=1e-3, K=3, A=A, B=B, eps=eps)
+    assert rc == 0 and np.max(np.abs(y3 - ref) / np.maximum(np.abs(ref), 1.0)) <= 1e-5
