@@ -297,3 +297,39 @@ def test_bruss_trajectory_vs_independent_radau():
     # the same solution
     rc, y3, _, _ = oracle.sbdf_integrate(y0, 200, kind=0, nx=nx, kx=c / dx, h=1e-3, K=3, A=A, B=B, eps=eps)
     assert rc == 0 and np.max(np.abs(y3 - ref) / np.maximum(np.abs(ref), 1.0)) <= 1e-5
+
+
+def test_bruss3d_trajectory_vs_independent_radau():
+    """The 3D problem of R19 (upwind along x, y, z, periodic; Gaussian IC with
+    per-axis σ = L/4): the oracle's SBDF2 against Radau IIA on the
+    semi-discrete system written out here, second-order convergence."""
+    from scipy.integrate import solve_ivp
+
+    n = 6
+    c, A, B, eps, alpha = PR["c"], PR["A"], PR["B"], PR["eps"], PR["alpha"]
+    d = 1.0 / n
+    ax = np.arange(n) * d
+    X, Y, Z = np.meshgrid(ax, ax, ax, indexing="ij")        # cell (i, j, k) = (x, y, z)
+    r2 = (X - 0.5) ** 2 + (Y - 0.5) ** 2 + (Z - 0.5) ** 2
+    p = alpha * np.exp(-r2 / (2 * 0.25 ** 2))
+    p = np.transpose(p, (2, 1, 0)).reshape(-1)                # index ((k ny + j) nx + i)
+    y0 = np.stack([A + p, B / A + p, 3.0 + p], 1).reshape(-1)
+    assert np.max(np.abs(y0 - oracle.bruss_ic(n, n, n))) <= 1e-15
+
+    def rhs(t, yy):
+        q = yy.reshape(n, n, n, 3)                            # [k, j, i, s]
+        adv = -c / d * ((q - np.roll(q, 1, axis=2)) + (q - np.roll(q, 1, axis=1)) + (q - np.roll(q, 1, axis=0)))
+        u, v, w = q[..., 0], q[..., 1], q[..., 2]
+        react = np.stack([A - (w + 1) * u + v * u * u, w * u - v * u * u, (B - w) / eps - w * u], -1)
+        return (adv + react).reshape(-1)
+
+    T = 0.1
+    ref = solve_ivp(rhs, (0.0, T), y0, method="Radau", rtol=1e-12, atol=1e-13).y[:, -1]
+    errs = []
+    for nsteps in (100, 200, 400):
+        rc, y, _, _ = oracle.sbdf_integrate(y0, nsteps, kind=0, nx=n, ny=n, nz=n, kx=c / d, ky=c / d, kz=c / d,
+                                            h=T / nsteps, newton_mode=2)
+        assert rc == 0
+        errs.append(np.max(np.abs(y - ref) / np.maximum(np.abs(ref), 1.0)))
+    assert errs[0] <= 1e-5, errs
+    assert 1.7 < math.log2(errs[0] / errs[1]) < 2.3 and 1.7 < math.log2(errs[1] / errs[2]) < 2.3, errs
