@@ -169,7 +169,7 @@ int enqueue_step(Stepper* S, bool first) {
 
   sunbw::FusedAdvection fa;
   const bool adv_in_kernel = o.fused && o.fused_advection && sunbw::bw_fused_advection(S->prob, y, &fa) &&
-                             G % 128 == 0;
+                             G % 128 == 0 && G <= INT32_MAX;
   // P > 1 with the single-kernel step: the halo plane travels on a side
   // stream while the interior tiles (local planes k >= 1) are computed; the
   // plane-0 tiles, which read it, run after the join (SURVEY §8(e) overlap)

@@ -215,3 +215,52 @@ def test_full_size_1e8_sampled(S, ctx):
     for j in range(8):
         Xj = host(X8[j])
         assert abs(d[j] - oracle.dot(xh, Xj)) <= 1e-12 * float(np.sum(np.abs(xh * Xj)))
+
+
+@pytest.mark.slow
+def test_max_size_beyond_int32_sampled(S, ctx):
+    """Largest size class: n = 2^31 + 37 elements (17.2 GB per vector), past
+    32-bit element indices and byte offsets — the N_Vector ops must index
+    with 64 bits (S:150 places no upper bound on n; SURVEY §8(d) C2 runs to
+    1e9).  Streaming ops: sampled indices bit-exact against the oracle
+    (counter generator, so the oracle draws the sampled inputs alone, the
+    last 4096 included).  Reductions: WRMS/Dot/MaxNorm against the oracle's
+    compensated sums taken over 2^27-element chunks and combined with
+    math.fsum (exact combination of the chunk results; DESIGN R6 bounds)."""
+    n = (1 << 31) + 37
+    free, _ = torch.cuda.mem_get_info()
+    if free < 80 * (1 << 30):
+        pytest.skip("needs ~75 GB of free device memory")
+    x = gen(1, n)
+    y = gen(2, n)
+    z = torch.empty_like(x)
+    vx, vy, vz = S.NVector(ctx, x), S.NVector(ctx, y), S.NVector(ctx, z)
+    idx = torch.cat([torch.arange(4096), torch.arange(n - 4096, n),
+                     torch.arange((1 << 31) - 2048, (1 << 31) + 37),
+                     torch.randint(0, n, (200_000,), generator=torch.Generator().manual_seed(11))])
+    xs = synth.uniform_at(1, idx, -1, 1).numpy()
+    ys = synth.uniform_at(2, idx, -1, 1).numpy()
+    S.N_VLinearSum(1.25, vx, -0.75, vy, vz)
+    assert_bits_equal(z[idx.cuda()], oracle.linear_sum(1.25, xs, -0.75, ys), "2^31+37 linear_sum")
+    S.N_VScale(-3.0, vx, vz)
+    assert_bits_equal(z[idx.cuda()], oracle.scale(-3.0, xs), "2^31+37 scale")
+    del y, vy
+    w = z                                    # reuse the buffer for the weights
+    w.copy_(gen(3, n, 0.5, 1.5))
+    vw = S.NVector(ctx, w)
+    got_w = S.N_VWrmsNorm(vx, vw)
+    got_d = S.N_VDotProd(vx, vw)
+    got_m = S.N_VMaxNorm(vx)
+    ctx.check("2^31+37 reductions")
+    ch = 1 << 27
+    sq, dd, ad, mx = [], [], [], 0.0
+    for s in range(0, n, ch):
+        xc, wc = host(x[s:s + ch]), host(w[s:s + ch])
+        sq.append(oracle.wsqrsum(xc, wc))
+        dd.append(oracle.dot(xc, wc))
+        ad.append(float(np.sum(np.abs(xc * wc))))
+        mx = max(mx, oracle.max_norm(xc))
+    ref_w = math.sqrt(math.fsum(sq) / n)
+    assert abs(got_w - ref_w) <= 1e-12 * ref_w, (got_w, ref_w)
+    assert abs(got_d - math.fsum(dd)) <= 1e-12 * math.fsum(ad), (got_d, math.fsum(dd))
+    assert got_m == mx
