@@ -1,0 +1,114 @@
+// Memory-side ceiling of the fused step's data movement, without its
+// arithmetic (diagnostic for DESIGN §11): the same persistent grid (740 CTAs
+// x 128 threads), 128-cell AoS tiles moved by bulk copies into a 2-stage
+// mbarrier ring and out by bulk stores from double-buffered shared tiles.
+//   mode 0: y_n + H_n in, y_{n+1} + H_{n+1} out          (4 streams, 96 B/cell)
+//   mode 1: mode 0 + the row-below and plane-below tiles  (the fused step's pattern)
+//   mode 2: mode 1 with a dependent fp64 chain of `chain` ops per cell
+// Prints us per launch and algorithmic GB/s (96 B/cell) per mode.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int kCells = 128, kTile = kCells * 3;
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void g2s(void* d, const void* s, uint32_t n, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(d)),
+               "l"(s), "r"(n), "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void s2g(void* d, const void* s, uint32_t n) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d), "r"(sa(s)), "r"(n) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+struct __align__(128) Smem {
+  double in[2][4][kTile];
+  double out[2][2][kTile];
+  uint64_t full[2];
+};
+
+__global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const double* h, double* z, double* ho,
+                                                      int64_t ntiles, int64_t row_tiles, int64_t plane_tiles,
+                                                      int mode, int chain) {
+  extern __shared__ __align__(128) unsigned char raw[];
+  Smem& S = *reinterpret_cast<Smem*>(raw);
+  const int t = threadIdx.x;
+  auto issue = [&](int64_t tile, int st) {
+    const bool nb = mode >= 1;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&S.full[st])),
+                 "r"((nb ? 4 : 2) * kTile * 8) : "memory");
+    g2s(S.in[st][0], y + tile * kTile, kTile * 8, &S.full[st]);
+    g2s(S.in[st][1], h + tile * kTile, kTile * 8, &S.full[st]);
+    if (nb) {
+      const int64_t ym = tile >= row_tiles ? tile - row_tiles : tile;
+      const int64_t zm = tile >= plane_tiles ? tile - plane_tiles : tile + ntiles - plane_tiles;
+      g2s(S.in[st][2], y + ym * kTile, kTile * 8, &S.full[st]);
+      g2s(S.in[st][3], y + zm * kTile, kTile * 8, &S.full[st]);
+    }
+  };
+  if (t == 0) {
+    for (int s = 0; s < 2; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&S.full[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int s = 0; s < 2; ++s)
+      if (blockIdx.x + s * (int64_t)gridDim.x < ntiles) issue(blockIdx.x + s * (int64_t)gridDim.x, s);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it & 1;
+    asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(
+                     sa(&S.full[st])), "r"((uint32_t)((it >> 1) & 1)) : "memory");
+    const int ob = it & 1;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      double a = S.in[st][0][3 * t + s], b = S.in[st][1][3 * t + s];
+      if (mode >= 1) a = __dadd_rn(a, __dadd_rn(S.in[st][2][3 * t + s], S.in[st][3][3 * t + s]));
+      if (mode == 2)
+        for (int c = 0; c < chain; ++c) a = __fma_rn(a, 0.999999, b);
+      S.out[ob][0][3 * t + s] = a;
+      S.out[ob][1][3 * t + s] = b;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+      s2g(z + tile * kTile, S.out[ob][0], kTile * 8);
+      s2g(ho + tile * kTile, S.out[ob][1], kTile * 8);
+      const int64_t nx = tile + 2 * (int64_t)gridDim.x;
+      if (nx < ntiles) issue(nx, st);
+    }
+  }
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int main() {
+  const int64_t n = 256, G = n * n * n, ntiles = G / kCells;
+  double *y, *h, *z, *ho;
+  const size_t bytes = (size_t)G * 3 * 8;
+  cudaMalloc(&y, bytes); cudaMalloc(&h, bytes); cudaMalloc(&z, bytes); cudaMalloc(&ho, bytes);
+  cudaMemset(y, 0, bytes); cudaMemset(h, 0, bytes);
+  const int smem = sizeof(Smem);
+  cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = nsm * 5;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  struct { int mode, chain; } cases[] = {{0, 0}, {1, 0}, {2, 32}, {2, 64}, {2, 128}, {2, 256}};
+  for (auto c : cases) {
+    for (int w = 0; w < 3; ++w)
+      k_tiles<<<grid, kCells, smem>>>(y, h, z, ho, ntiles, 2, 512, c.mode, c.chain);
+    cudaEventRecord(e0);
+    const int reps = 20;
+    for (int r = 0; r < reps; ++r)
+      k_tiles<<<grid, kCells, smem>>>((r & 1) ? z : y, (r & 1) ? ho : h, (r & 1) ? y : z, (r & 1) ? h : ho, ntiles,
+                                      2, 512, c.mode, c.chain);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double us = ms * 1e3 / reps;
+    printf("mode %d chain %3d (3 chains/thread): %7.1f us/launch  %6.0f GB/s algorithmic (96 B/cell)  err=%s\n",
+           c.mode, c.chain, us, 96.0 * G / (us * 1e-6) / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
