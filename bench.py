@@ -43,6 +43,7 @@ BYTES_PER_CELL = {
 WRMS_FUSED_BYTES = 0        # the fused path's fold reads only per-CTA partials
 NUM_SMS = 148
 FP64_LANES_PER_SM = 64
+FP64_SUSTAINED_TOPS = 12.3          # T fp64 op/s sustained by DFMA chains in the fused grid structure (r01i)
 
 
 def sm_max_mhz():
@@ -467,7 +468,13 @@ def main():
             roofline["fp64"] = {"achieved": round(a64, 2), "peak": round(p64, 2), "unit": "Top/s",
                                 "frac": round(a64 / p64, 4), "ops_per_cell": ops,
                                 "peak_source": "148 SMs x 64 FP64 lanes/clk (profiles/r01d_fp64_latency.txt: "
-                                               "0.49 fp64 warp-instr/clk/SMSP) x sm_max_mhz"}
+                                               "0.49 fp64 warp-instr/clk/SMSP) x sm_max_mhz",
+                                # context: what independent DFMA chains sustain in the
+                                # same grid/tile/TMA structure (DESIGN §6 calibration)
+                                "sustained": FP64_SUSTAINED_TOPS,
+                                "frac_of_sustained": round(a64 / FP64_SUSTAINED_TOPS, 4),
+                                "sustained_source": "profiles/r01i_tile_streams.txt "
+                                                    "(tools/microbench/tile_streams.cu, 3 x 256 DFMA/cell)"}
     # bytes per step of this mode; the composed path's are SURVEY §8(d)'s
     # 820 + 388 K per cell, the fused step's 96 per cell (R28)
     step_bytes = sum(BYTES_PER_CELL[k] * G * v["launches"] for k, v in kernels.items()
