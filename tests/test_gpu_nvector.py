@@ -228,6 +228,7 @@ def test_max_size_beyond_int32_sampled(S, ctx):
     compensated sums taken over 2^27-element chunks and combined with
     math.fsum (exact combination of the chunk results; DESIGN R6 bounds)."""
     n = (1 << 31) + 37
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < 80 * (1 << 30):
         pytest.skip("needs ~75 GB of free device memory")
@@ -264,3 +265,5 @@ def test_max_size_beyond_int32_sampled(S, ctx):
     assert abs(got_w - ref_w) <= 1e-12 * ref_w, (got_w, ref_w)
     assert abs(got_d - math.fsum(dd)) <= 1e-12 * math.fsum(ad), (got_d, math.fsum(dd))
     assert got_m == mx
+    del x, z, w, vx, vz, vw
+    torch.cuda.empty_cache()
