@@ -186,12 +186,12 @@ METRIC = ("advection-reaction throughput, cell time-steps/s (3D Brusselator, 256
           "SBDF2 + K=3 block-LU Newton, fp64)")
 
 
-def workload_config(world, mode, n_ax=256):
+def workload_config(world, mode, n_ax=256, numerics=None):
     """The `config` object of both arms (BASELINE configs[4], one slab per GPU)."""
     return {"workload": "C5: 3D Brusselator advection-reaction, 256^3 cells per GPU "
                         "(configs[4]; N=1 is one slab)",
             "cells_per_gpu": n_ax ** 3, "global_grid": [n_ax, n_ax, n_ax * world],
-            "K": 3, "h": 1e-3, "mode": mode, "parallelism": f"z-slab x{world}",
+            "K": 3, "h": 1e-3, "mode": mode, "numerics": numerics, "parallelism": f"z-slab x{world}",
             "l2": "inputs larger than L2 (state 403 MB per vector)"}
 
 
@@ -363,6 +363,9 @@ def main():
     ap.add_argument("--impl", default="sunbw", choices=["sunbw", "reference"])
     ap.add_argument("--mode", default="fused", choices=["fused", "composed"])
     ap.add_argument("--cells", type=int, default=256, help="cells per axis per GPU slab")
+    ap.add_argument("--numerics", default="contracted", choices=["contracted", "exact"],
+                    help="fused cell step: FMA-contracted (rel 1e-9 parity, DESIGN R30) or the "
+                         "bit-exact RN sequence")
     ap.add_argument("--no-ops", action="store_true", help="skip the C2 N_Vector op point")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--ref-planes", type=int, default=8)
@@ -401,7 +404,9 @@ def main():
     fused = args.mode == "fused"
     # graph replay of the step at N = 1; eager launches when NCCL is in the
     # step (halo on a side stream), which is not exercised under capture here
-    st = S.Stepper(P, vy0, S.stepper_options(h=1e-3, K=3, use_graph=world == 1, timing=True, fused=fused))
+    numerics = 1 if (fused and args.numerics == "contracted") else 0
+    st = S.Stepper(P, vy0, S.stepper_options(h=1e-3, K=3, use_graph=world == 1, timing=True, fused=fused,
+                                             numerics=numerics))
     rc, _ = st.advance(args.warmup)
     assert rc == 0, rc
     st.kernel_times(reset=True)
@@ -526,7 +531,7 @@ def main():
             "steps_per_s": args.steps / (ms * 1e-3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper's Gaussian IC, P:376-382, on the 3D grid)",
-            "config": workload_config(world, args.mode, n_ax),
+            "config": workload_config(world, args.mode, n_ax, args.numerics if fused else "exact"),
             "roofline": roofline, "step_bytes": step_bytes, "composed_equiv_bytes_per_step": (820 + 388 * 3) * G,
             "step_GB/s": round(step_bytes / (ms / args.steps * 1e-3) / 1e9, 1),
             "kernels": kernels, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,

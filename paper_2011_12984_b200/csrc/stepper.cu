@@ -44,7 +44,7 @@ int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, do
                  double rtol, double atol, const double* y, const double* fE, const double* hin,
                  double* hout, double* z, double* partials, unsigned long long* d_first,
                  int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end,
-                 const FusedFold* fold, bool gj);
+                 const FusedFold* fold, int solver);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
                double* d_min, double* d_nu, int* d_err);
 int fused_finalize_pending(SUNBW_Context ctx, double* pending, int K, int64_t nglobal, double* d_min,
@@ -194,6 +194,7 @@ int enqueue_step(Stepper* S, bool first) {
 
   if (o.fused) {
     int nb = 0, nb2 = 0;
+    const int solver = o.numerics == 1 ? 2 : (o.linsol == 2 ? 1 : 0);
     // partials are folded by the step's last CTA unless a blocking
     // allreduce must sit between fold and finalisation (P > 1, not deferred)
     const bool fold_in_kernel = S->deferred || ctx_nranks(ctx) <= 1;
@@ -210,7 +211,7 @@ int enqueue_step(Stepper* S, bool first) {
       {
         Timed t(S, BW_K_FUSED_NEWTON);
         TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
-                                S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr, o.linsol == 2));
+                                S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr, solver));
       }
       if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
       fold.prev_parts = nb;
@@ -218,13 +219,13 @@ int enqueue_step(Stepper* S, bool first) {
         Timed t(S, BW_K_FUSED_NEWTON);
         TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
                                 S->d_partials + (int64_t)nb * (o.K + 1), S->d_first, &nb2, &fa, 0, tpp,
-                                fk, o.linsol == 2));
+                                fk, solver));
       }
     } else {
       Timed t(S, BW_K_FUSED_NEWTON);
       TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y,
                               adv_in_kernel ? nullptr : fE_n, fEp, fE, z, S->d_partials, S->d_first, &nb,
-                              adv_in_kernel ? &fa : nullptr, 0, -1, fk, o.linsol == 2));
+                              adv_in_kernel ? &fa : nullptr, 0, -1, fk, solver));
     }
     if (!fold_in_kernel) {
       Timed t(S, BW_K_WRMS);
@@ -410,7 +411,9 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
     return SUNBW_ERR_ARG;
   if (opt->linsol < 0 || opt->linsol > 2 || (opt->linsol == 1 && (opt->maxl < 1 || opt->maxl > 60)))
     return SUNBW_ERR_ARG;
+  if (opt->numerics < 0 || opt->numerics > 1) return SUNBW_ERR_ARG;
   if (opt->fused && (opt->newton_mode != 0 || opt->K > 8 || opt->linsol == 1)) return SUNBW_ERR_UNSUPPORTED;
+  if (opt->fused && opt->numerics == 1 && opt->linsol != 0) return SUNBW_ERR_UNSUPPORTED;
   SUNBW_Context ctx = y0->ctx;
   int64_t G = sunbw::bw_local_cells(prob);
   if (y0->local_len != 3 * G) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
@@ -486,7 +489,8 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
     // per-step kernels
     {
       Timed t(S, BW_K_FUSED_NEWTON);
-      TRY(sunbw::fused_multistep(ctx, S->prob, S->sg, S->G, S->step == 0, nsteps, S->opt.K, S->opt.linsol == 2,
+      TRY(sunbw::fused_multistep(ctx, S->prob, S->sg, S->G, S->step == 0, nsteps, S->opt.K,
+                                 S->opt.numerics == 1 ? 2 : (S->opt.linsol == 2 ? 1 : 0),
                                  S->opt.h, S->opt.rtol, S->opt.atol, S->y[S->iy], S->fE[S->ifep], S->y[S->iz],
                                  S->fE[S->ife], S->d_scal, S->d_err, S->d_first, S->nglobal));
     }

@@ -178,7 +178,7 @@ struct SmallGeom {
 };
 bool bw_small_geometry(void* prob, SmallGeom* g);
 int fused_multistep(SUNBW_Context ctx, void* prob, const SmallGeom& gm, int64_t G, bool first, int64_t nsteps,
-                    int K, bool gj, double h, double rtol, double atol, const double* y, const double* hin,
+                    int K, int solver, double h, double rtol, double atol, const double* y, const double* hin,
                     double* y_out, double* hout, double* d_scal, int* d_err, unsigned long long* d_first,
                     int64_t nglobal);
 

@@ -46,7 +46,7 @@ class BW_StepperOptions(C.Structure):
                 ("rtol", _D), ("atol", _D), ("use_graph", C.c_int32), ("timing", C.c_int32),
                 ("fused", C.c_int32), ("fused_advection", C.c_int32),
                 ("linsol", C.c_int32), ("maxl", C.c_int32), ("lin_tol", _D),
-                ("single_step_launches", C.c_int32), ("pad_", C.c_int32)]
+                ("single_step_launches", C.c_int32), ("numerics", C.c_int32)]
 
 
 class BW_StepperStats(C.Structure):
@@ -557,10 +557,12 @@ def BW_ReactionJacobian(P: Problem, y: NVector, J: SUNMatrix) -> int:
 def stepper_options(h=1e-3, newton_mode=0, K=3, tol_nl=1e-3, rtol=1e-6, atol=1e-9,
                     use_graph=True, timing=False, fused=False,
                     fused_advection=True, linsol=0, maxl=5, lin_tol=1e-10,
-                    single_step_launches=False) -> BW_StepperOptions:
+                    single_step_launches=False, numerics=0) -> BW_StepperOptions:
+    """numerics (fused mode): 0 bit-exact, 1 contracted (FMA) cell step held
+    to relative 1e-9 (DESIGN R30)."""
     return BW_StepperOptions(h, newton_mode, K, tol_nl, rtol, atol, int(use_graph), int(timing),
                              int(fused), int(fused_advection), linsol, maxl, lin_tol,
-                             int(single_step_launches), 0)
+                             int(single_step_launches), int(numerics))
 
 
 class Stepper:
