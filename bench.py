@@ -43,7 +43,39 @@ BYTES_PER_CELL = {
 WRMS_FUSED_BYTES = 0        # the fused path's fold reads only per-CTA partials
 NUM_SMS = 148
 FP64_LANES_PER_SM = 64
-FP64_SUSTAINED_TOPS = 12.3          # T fp64 op/s sustained by DFMA chains in the fused grid structure (r01i)
+
+
+# sources that compile into the fused step kernel: profiles/ncu_traffic.json
+# entries are keyed by their hash (a stale ncu number is never reported)
+KERNEL_SOURCES = ["paper_2011_12984_b200/csrc/fused.cu", "paper_2011_12984_b200/csrc/pipeline.cuh",
+                  "paper_2011_12984_b200/csrc/sunbw_internal.h", "paper_2011_12984_b200/csrc/sunbw_device.cuh",
+                  "include/sunbw.h", "paper_2011_12984_b200/_build.py"]
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def kernel_src_sha16():
+    import hashlib
+    h = hashlib.sha256()
+    for rel in KERNEL_SOURCES:
+        with open(os.path.join(ROOT, rel), "rb") as f:
+            h.update(rel.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_entry(kernel: str, variant: str):
+    """ncu numbers of this kernel variant if they were captured from the
+    current sources, else None (reported as stale)."""
+    try:
+        with open(TRAFFIC_JSON) as f:
+            entries = json.load(f).get("entries", {})
+    except (OSError, ValueError):
+        return None, "missing"
+    e = entries.get(f"{kernel}/{variant}")
+    if not e:
+        return None, "missing"
+    if e.get("src_sha16") != kernel_src_sha16():
+        return None, f"stale (captured from sources {e.get('src_sha16')}, now {kernel_src_sha16()})"
+    return e, "current"
 
 
 def sm_max_mhz():
@@ -148,35 +180,77 @@ def max_over_ranks(ms: float, dist, world: int, device) -> float:
     return float(t.item())
 
 
-def run_reference(args, world, rank):
-    """The serial CPU oracle, as it stands, on a bounded sample of the same
-    workload: a 256 x 256 x nzs slab (periodic), same parameters, fixed K."""
-    if rank != 0:
-        return
+# ------------------------------------------------- the oracle on the host
+REF_PLANES = 8              # oracle sample: a 256 x 256 x 8 slab (1/32 of the 256^3 slab)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class PinnedCore:
+    """One protocol for every oracle timing (both arms): the calling thread
+    pinned to one host core (the last one it may use), the CPU model and the
+    available core count recorded; the previous affinity restored after."""
+
+    def __enter__(self):
+        self.prev = os.sched_getaffinity(0)
+        self.available = len(self.prev)
+        self.core = max(self.prev)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.prev)
+
+    def describe(self):
+        return {"cores": 1, "pinned_core": self.core, "available_cores": self.available,
+                "cpu_model": cpu_model(), "threads": "1 (serial oracle, pinned)"}
+
+
+def oracle_c5_sample(steps, warmup=0, planes=REF_PLANES):
+    """The oracle on the bench workload's sample: a 256 x 256 x planes
+    periodic slab with the C5 parameters, SBDF + K = 3; returns (cell-steps/s,
+    seconds, rc).  Call inside PinnedCore."""
     import oracle
     oracle.build()
     nx = ny = 256
-    nzs = args.ref_planes
-    L = 1.0
-    k = 0.01 / (L / nx)
-    y0 = oracle.bruss_ic(nx, ny, nzs, L, L, L * nzs / 256)
-    kw = dict(kind=0, K=3, nx=nx, ny=ny, nz=nzs, kx=k, ky=k, kz=k, h=1e-3)
-    if args.warmup:
-        oracle.sbdf_integrate(y0, args.warmup, **kw)
+    k = 0.01 * nx
+    y0 = oracle.bruss_ic(nx, ny, planes, 1.0, 1.0, planes / 256)
+    kw = dict(kind=0, K=3, nx=nx, ny=ny, nz=planes, kx=k, ky=k, kz=k, h=1e-3)
+    if warmup:
+        oracle.sbdf_integrate(y0, warmup, **kw)
     t0 = time.perf_counter()
-    rc, _, _, _ = oracle.sbdf_integrate(y0, args.steps, **kw)
+    rc, _, _, _ = oracle.sbdf_integrate(y0, steps, **kw)
     dt = time.perf_counter() - t0
-    cells = nx * ny * nzs
-    v = cells * args.steps / dt
-    sample = f"{nx}x{ny}x{nzs} cells (1/{256 // nzs} of a 256^3 slab), {args.steps} SBDF2 steps, K=3"
+    return nx * ny * planes * steps / dt, dt, rc
+
+
+def run_reference(args, world, rank):
+    """The serial CPU oracle, as it stands, pinned to one core, on a bounded
+    sample of the same workload: a 256 x 256 x 8 slab (periodic), same
+    parameters, fixed K; W warm-up steps, then K timed steps."""
+    if rank != 0:
+        return
+    with PinnedCore() as pc:
+        v, dt, rc = oracle_c5_sample(args.steps, args.warmup, planes=args.ref_planes)
+        desc = pc.describe()
+    sample = (f"256x256x{args.ref_planes} cells (1/{256 // args.ref_planes} of a 256^3 slab), "
+              f"{args.steps} SBDF2 steps, K=3")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "cell-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (paper IC, P:376-382)",
         "config": workload_config(world, "oracle (serial CPU, bounded sample: see cpu_baseline)"),
-        "cpu_baseline": {"value": v, "unit": "cell-steps/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+        "cpu_baseline": dict({"value": v, "unit": "cell-steps/s", "kind": "oracle", "sample": sample}, **desc),
         "e2e": {"value": v, "unit": "cell-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "rc": rc,
     }), flush=True)
@@ -195,46 +269,133 @@ def workload_config(world, mode, n_ax=256, numerics=None):
             "l2": "inputs larger than L2 (state 403 MB per vector)"}
 
 
-def cpu_baseline_sample(planes=64, steps=15):
-    """Oracle on the GPU box's host, one core, bounded sample (~10 s)."""
+def _c4_chunk(args):
+    """k-process estimate worker: the oracle on a chunk of C4-shaped
+    independent reaction cells (its own process, its own core)."""
+    core, G, steps = args
+    os.sched_setaffinity(0, {core})
+    import numpy as np
+    import oracle
+    import synth
+    u = synth.uniform(synth.S_CELL, G, 0.0, 1.0).numpy()
+    y0 = np.stack([1.0 + 0.1 * u, 3.5 + 0.1 * u, 3.0 + 0.1 * u], 1).reshape(-1)
+    t0 = time.perf_counter()
+    oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=G, reaction_only=True, h=1e-3)
+    return G * steps, time.perf_counter() - t0
+
+
+def cpu_baseline_sample(steps=20, warmup=5):
+    """The oracle on the GPU box's host (rank 0, N = 1), the reference
+    arm's protocol (PinnedCore, same 256x256x8 sample) for ~10 s, plus the
+    small configs (C1 in full, C3 for 2 steps) and a labelled estimate of k
+    concurrent oracle processes on C4 cell chunks (the analog of the paper's
+    MPI+serial baseline)."""
     import oracle
     oracle.build()
-    nx = ny = 256
-    k = 0.01 * nx
-    y0 = oracle.bruss_ic(nx, ny, planes, 1.0, 1.0, planes / 256)
-    t0 = time.perf_counter()
-    oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=nx, ny=ny, nz=planes, kx=k, ky=k, kz=k, h=1e-3)
-    dt = time.perf_counter() - t0
-    return {"value": nx * ny * planes * steps / dt, "unit": "cell-steps/s", "cores": 1,
-            "kind": "oracle",
-            "sample": f"256x256x{planes} cells, {steps} SBDF steps (K=3), 1 host thread, {dt:.1f} s"}
+    # the main sample: the reference arm itself (`--impl reference`, same
+    # protocol, fresh process), so the two oracle timings cannot diverge
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps",
+                        str(steps), "--warmup", str(warmup)], capture_output=True, text=True, timeout=900,
+                       env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})
+    ref = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    out = dict(ref["cpu_baseline"])
+    out["protocol"] = f"python bench.py --impl reference --steps {steps} --warmup {warmup} (subprocess)"
+    with PinnedCore() as pc:
+        t0 = time.perf_counter()
+        oracle.sbdf_integrate(oracle.bruss_ic(64), 1000, kind=0, K=3, nx=64, kx=0.01 * 64, h=1e-3)
+        c1 = 1000 / (time.perf_counter() - t0)
+        n3 = 128
+        y3 = oracle.bruss_ic(n3, n3, n3)
+        t0 = time.perf_counter()
+        oracle.sbdf_integrate(y3, 2, kind=0, K=3, nx=n3, ny=n3, nz=n3, kx=0.01 * n3, ky=0.01 * n3,
+                              kz=0.01 * n3, h=1e-3)
+        c3 = 2 / (time.perf_counter() - t0)
+    out["other_configs"] = {"C1_steps_per_s": round(c1, 1), "C3_steps_per_s": round(c3, 4)}
+    try:
+        import multiprocessing as mp
+        cores = sorted(os.sched_getaffinity(0))
+        Gc, sc = 200_000, 10
+        with mp.get_context("spawn").Pool(len(cores)) as pool:
+            res = pool.map(_c4_chunk, [(c, Gc, sc) for c in cores])
+        out["k_process_estimate"] = {
+            "value": sum(r[0] for r in res) / max(r[1] for r in res), "unit": "cell-steps/s",
+            "processes": len(cores), "kind": "estimate",
+            "sample": f"{len(cores)} concurrent oracle processes x {Gc} C4 reaction cells x {sc} steps, "
+                      "one core each (aggregate / slowest)"}
+    except Exception as e:  # pragma: no cover
+        out["k_process_estimate"] = {"unavailable": str(e)[:200]}
+    return out
+
+
+NV_OPS = {   # name: (bytes per element, vectors: x, y/w, id, z, X_j, Z_j)
+    "N_VLinearSum": 24, "N_VScale": 16, "N_VProd": 24, "N_VDiv": 24, "N_VWrmsNorm": 16,
+    "N_VWrmsNormMask": 24, "N_VDotProd": 16, "N_VLinearCombination_8": 72, "N_VScaleAddMulti_8": 136,
+    "N_VDotProdMulti_8": 72}
 
 
 def nvector_ops(S, ctx, torch, peak, n=100_000_000, reps=20):
-    """C2 sweep point at n = 1e8 through the public N_V* calls (inputs
-    800 MB each, > L2).  Reductions include their host return."""
+    """C2 sweep point through the public N_V* calls, every op the north star
+    names (+ the masked WRMS): inputs > L2; reductions include their host
+    return.  Vectors are drawn in 1e8-element chunks and allocated
+    per op, so the 1e9 point (ScaleAddMulti x8: 17 vectors, 136 GB) fits."""
     import synth
-    out = {}
-    dev = "cuda"
-    x = synth.uniform(1, n, -1, 1, device=dev)
-    y = synth.uniform(2, n, -1, 1, device=dev)
-    w = synth.uniform(3, n, 0.5, 1.5, device=dev)
-    z = torch.empty_like(x)
-    X = [synth.uniform(32 + j, n, -1, 1, device=dev) for j in range(8)]
-    vx, vy, vw, vz = (S.NVector(ctx, t) for t in (x, y, w, z))
-    vX = [S.NVector(ctx, t) for t in X]
-    c = [(j + 1) / 8 for j in range(8)]
-    ops = {
-        "N_VLinearSum": (lambda: S.N_VLinearSum(1.25, vx, -0.75, vy, vz), 24),
-        "N_VScale": (lambda: S.N_VScale(0.5, vx, vz), 16),
-        "N_VProd": (lambda: S.N_VProd(vx, vy, vz), 24),
-        "N_VWrmsNorm": (lambda: S.N_VWrmsNorm(vx, vw), 16),
-        "N_VDotProd": (lambda: S.N_VDotProd(vx, vy), 16),
-        "N_VLinearCombination_8": (lambda: S.N_VLinearCombination(c, vX, vz), 72),
-        "N_VDotProdMulti_8": (lambda: S.N_VDotProdMulti(vx, vX), 72),
-    }
     stream = torch.cuda.current_stream()
-    for name, (fn, bpe) in ops.items():
+    chunk = 100_000_000
+
+    def draw(stream_id, lo, hi):
+        v = torch.empty(n, dtype=torch.float64, device="cuda")
+        for a in range(0, n, chunk):
+            b = min(n, a + chunk)
+            v[a:b] = synth.uniform_at(stream_id, torch.arange(a, b, device="cuda"), lo, hi)
+        return v
+
+    c8 = [(j + 1) / 8 for j in range(8)]
+    a8 = [1 - j / 16 for j in range(8)]
+    out = {}
+
+    def run_op(name, bpe):              # every vector of the op dies with this frame
+        keep = []
+
+        def vec(stream_id, lo=-1.0, hi=1.0):
+            keep.append(draw(stream_id, lo, hi))
+            return S.NVector(ctx, keep[-1])
+
+        def empty():
+            keep.append(torch.empty(n, dtype=torch.float64, device="cuda"))
+            return S.NVector(ctx, keep[-1])
+
+        x = vec(synth.S_X)
+        if name == "N_VLinearSum":
+            y, z = vec(synth.S_Y), empty()
+            fn = lambda: S.N_VLinearSum(1.25, x, -0.75, y, z)
+        elif name == "N_VScale":
+            z = empty()
+            fn = lambda: S.N_VScale(0.5, x, z)
+        elif name == "N_VProd":
+            y, z = vec(synth.S_Y), empty()
+            fn = lambda: S.N_VProd(x, y, z)
+        elif name == "N_VDiv":
+            y, z = vec(synth.S_Y, 0.5, 1.5), empty()
+            fn = lambda: S.N_VDiv(x, y, z)
+        elif name == "N_VWrmsNorm":
+            w = vec(synth.S_W, 0.5, 1.5)
+            fn = lambda: S.N_VWrmsNorm(x, w)
+        elif name == "N_VWrmsNormMask":
+            w, idm = vec(synth.S_W, 0.5, 1.5), vec(synth.S_ID, 0.0, 1.0)
+            fn = lambda: S.N_VWrmsNormMask(x, w, idm)
+        elif name == "N_VDotProd":
+            y = vec(synth.S_Y)
+            fn = lambda: S.N_VDotProd(x, y)
+        elif name == "N_VLinearCombination_8":
+            X, z = [vec(synth.S_XJ + j) for j in range(8)], empty()
+            fn = lambda: S.N_VLinearCombination(c8, X, z)
+        elif name == "N_VScaleAddMulti_8":
+            Y = [vec(synth.S_YJ + j) for j in range(8)]
+            Z = [empty() for _ in range(8)]
+            fn = lambda: S.N_VScaleAddMulti(a8, x, Y, Z)
+        else:
+            X = [vec(synth.S_XJ + j) for j in range(8)]
+            fn = lambda: S.N_VDotProdMulti(x, X)
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -246,9 +407,15 @@ def nvector_ops(S, ctx, torch, peak, n=100_000_000, reps=20):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         gbs = bpe * n / (ms * 1e-3) / 1e9
-        out[name] = {"us": round(ms * 1e3, 1), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4)}
+        return {"us": round(ms * 1e3, 1), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4),
+                "bytes_per_elem": bpe}
+
+    for name, bpe in NV_OPS.items():
+        out[name] = run_op(name, bpe)
+        torch.cuda.empty_cache()
     ctx.check("nvector ops")
-    del X, vX
+    out["_protocol"] = (f"n = {n:.0e}, {reps} timed calls after 3 warm-up, CUDA events; mask id ~ U[0,1) "
+                        "(> 0 everywhere: all terms summed); coefficients dyadic (SURVEY 8(d))")
     return out
 
 
@@ -368,7 +535,7 @@ def main():
                          "bit-exact RN sequence")
     ap.add_argument("--no-ops", action="store_true", help="skip the C2 N_Vector op point")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
-    ap.add_argument("--ref-planes", type=int, default=8)
+    ap.add_argument("--ref-planes", type=int, default=REF_PLANES)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "sunbw":
         args.warmup = 3
@@ -450,36 +617,27 @@ def main():
                          "share": round(kms / ms_local, 4), "GB/s": round(ach, 1)}
     dom = max(kernels, key=lambda k: kernels[k]["ms_total"] if BYTES_PER_CELL.get(k) else -1)
     ach = kernels[dom]["GB/s"]
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if n_ax == 256 and os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get(dom)        # ncu dram read+write per launch, same workload
+    variant = (args.numerics if fused else "exact") if dom == "fused_newton" else "composed"
+    ent, ent_state = ncu_entry(dom, variant) if n_ax == 256 else (None, "not the bench size")
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic, "kernel": dom,
-                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, this workload)",
+                "frac": round(ach / peak, 4), "traffic": ent["dram_bytes"] if ent else None, "kernel": dom,
+                "traffic_source": f"profiles/ncu_traffic.json [{dom}/{variant}]: {ent_state}"
+                                  + (f", {ent['source']}" if ent else ""),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                 else "fallback (B200_PROFILING.md)",
-                "bytes_per_launch": BYTES_PER_CELL[dom] * G}
-    if fused and n_ax == 256 and os.path.exists(tpath):
+                "bytes_per_launch": BYTES_PER_CELL[dom] * G,
+                "bytes_per_unit": {"unit": "cell", "bytes": BYTES_PER_CELL[dom]}}
+    if ent and ent.get("fp64_per_cell"):
         # the fused step is as much an fp64-ALU kernel as an HBM one
         # (DESIGN.md §6): its fp64-pipe instructions per cell (ncu, same
-        # workload) against 148 SMs x 64 FP64 lanes x the max SM clock
-        with open(tpath) as f:
-            ops = json.load(f).get("fused_newton_fp64_per_cell")
-        if ops:
-            a64 = ops * G / (kernels[dom]["us_avg"] * 1e-6) / 1e12
-            p64 = FP64_LANES_PER_SM * NUM_SMS * sm_max_mhz() * 1e6 / 1e12
-            roofline["fp64"] = {"achieved": round(a64, 2), "peak": round(p64, 2), "unit": "Top/s",
-                                "frac": round(a64 / p64, 4), "ops_per_cell": ops,
-                                "peak_source": "148 SMs x 64 FP64 lanes/clk (profiles/r01d_fp64_latency.txt: "
-                                               "0.49 fp64 warp-instr/clk/SMSP) x sm_max_mhz",
-                                # context: what independent DFMA chains sustain in the
-                                # same grid/tile/TMA structure (DESIGN §6 calibration)
-                                "sustained": FP64_SUSTAINED_TOPS,
-                                "frac_of_sustained": round(a64 / FP64_SUSTAINED_TOPS, 4),
-                                "sustained_source": "profiles/r01i_tile_streams.txt "
-                                                    "(tools/microbench/tile_streams.cu, 3 x 256 DFMA/cell)"}
+        # sources and workload) against 148 SMs x 64 FP64 lanes x the max SM clock
+        ops = ent["fp64_per_cell"]
+        a64 = ops * G / (kernels[dom]["us_avg"] * 1e-6) / 1e12
+        p64 = FP64_LANES_PER_SM * NUM_SMS * sm_max_mhz() * 1e6 / 1e12
+        roofline["fp64"] = {"achieved": round(a64, 2), "peak": round(p64, 2), "unit": "Top/s",
+                            "frac": round(a64 / p64, 4), "ops_per_cell": ops,
+                            "peak_source": "148 SMs x 64 FP64 lanes/clk (profiles/r01d_fp64_latency.txt: "
+                                           "0.49 fp64 warp-instr/clk/SMSP) x sm_max_mhz"}
     # bytes per step of this mode; the composed path's are SURVEY §8(d)'s
     # 820 + 388 K per cell, the fused step's 96 per cell (R28)
     step_bytes = sum(BYTES_PER_CELL[k] * G * v["launches"] for k, v in kernels.items()
@@ -509,20 +667,24 @@ def main():
            "h2d_bytes_per_step": state_bytes / args.steps, "d2h_bytes_per_step": state_bytes / args.steps,
            "note": "pinned H2D of y0 + Advance(K) + D2H of y_K through the C ABI, timed with CUDA events"}
 
-    ops = None
+    ops = ops_1e9 = latency = None
     if rank == 0 and world == 1 and not args.no_ops:
         st.destroy()
         P.destroy()
         del y0, yout, ydev
         torch.cuda.empty_cache()
         ops = nvector_ops(S, ctx, torch, peak)
+        ops_1e9 = nvector_ops(S, ctx, torch, peak, n=1_000_000_000, reps=3)
+        latency = dict(zip(("eager_us_per_launch", "graph_us_per_node", "host_launch_sync_roundtrip_us"),
+                           (round(v, 3) for v in S.probe_launch_latency(ctx, 100_000))))
+        latency["protocol"] = "1e5 empty kernels (P:233-237 launch overhead; V100 ~8 us)"
     configs = None
     if rank == 0 and world == 1 and not args.no_ops:
         torch.cuda.empty_cache()
         configs = other_configs(S, ctx, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample()
+        cpu = cpu_baseline_sample(min(args.steps, 60), max(args.warmup, 3))
 
     if rank == 0:
         line = {
@@ -535,7 +697,8 @@ def main():
             "roofline": roofline, "step_bytes": step_bytes, "composed_equiv_bytes_per_step": (820 + 388 * 3) * G,
             "step_GB/s": round(step_bytes / (ms / args.steps * 1e-3) / 1e9, 1),
             "kernels": kernels, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "cpu_baseline": cpu, "nvector_ops_1e8": ops, "other_configs": configs,
+            "cpu_baseline": cpu, "nvector_ops_1e8": ops, "nvector_ops_1e9": ops_1e9,
+            "launch_latency": latency, "other_configs": configs,
             "newton_iters": stats["newton_iters"],
         }
         print(json.dumps(line), flush=True)

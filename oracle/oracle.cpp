@@ -834,7 +834,11 @@ int oracle_ark_integrate(const OracleArkParams* AP, double* y, OracleArkStats* s
   // (accumulated rounding of t; DESIGN R26)
   while (AP->t_end - t > 1e-12 * std::fmax(1.0, std::fabs(AP->t_end))) {
     if (attempts++ >= AP->max_steps) { st->t = t; st->h_last = h; return 1; }
-    if (t + h > AP->t_end) h = AP->t_end - t;
+    // a step shortened to land on t_end does not shrink the controller's
+    // next proposal (DESIGN R26): the unclipped h is kept for after it
+    const double h_unclipped = h;
+    const bool clipped = t + h > AP->t_end;
+    if (clipped) h = AP->t_end - t;
     if (h < 1e-14 * (1.0 + t)) { st->t = t; st->h_last = h; return 2; }
     // ewt from y_n
     oracle_abs(n, y, tmp.data());
@@ -907,6 +911,7 @@ int oracle_ark_integrate(const OracleArkParams* AP, double* y, OracleArkStats* s
       t += h;
       st->accepted++;
       h *= std::fmin(5.0, std::fmax(0.2, fac));
+      if (clipped) h = std::fmax(h, h_unclipped);
     } else {
       st->rejected_err++;
       h *= std::fmin(1.0, std::fmax(0.2, fac));

@@ -125,6 +125,8 @@ int attempt(Ark* A, int* nl_ok, double* dsm) {
       TRY(sunbw::scale_add_identity(ctx, G, 3, -hg, A->M));
       TRY(sunbw::lu_factor(ctx, G, 3, A->M, A->piv, A->d_first));
       A->st.setups++;
+      // a zero pivot on any rank recomputes the step on every rank
+      TRY(sunbw::or_flags_over_ranks(ctx, A->d_first, nullptr));
       unsigned long long f = 0;
       if (cudaMemcpyAsync(&f, A->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
           cudaStreamSynchronize(ctx->stream) != cudaSuccess)
@@ -216,7 +218,11 @@ extern "C" int BW_ArkEvolve(void* ark, double t_end, N_Vector y_out, BW_ArkStats
   int attempts = 0;
   while (t_end - A->t > 1e-12 * std::fmax(1.0, std::fabs(t_end))) {
     if (attempts++ >= A->opt.max_steps) { rc = 1; break; }
-    if (A->t + A->h > t_end) A->h = t_end - A->t;
+    // a step shortened to land on t_end does not shrink the next proposal
+    // (DESIGN R26): the unclipped h is restored after it if larger
+    const double h_unclipped = A->h;
+    const bool clipped = A->t + A->h > t_end;
+    if (clipped) A->h = t_end - A->t;
     if (A->h < 1e-14 * (1.0 + A->t)) { rc = 2; break; }
     int nl_ok = 1;
     double dsm = 0.0;
@@ -234,6 +240,7 @@ extern "C" int BW_ArkEvolve(void* ark, double t_end, N_Vector y_out, BW_ArkStats
       A->t += A->h;
       A->st.accepted++;
       A->h *= std::fmin(5.0, std::fmax(0.2, fac));
+      if (clipped) A->h = std::fmax(A->h, h_unclipped);
     } else {
       A->st.rejected_err++;
       A->h *= std::fmin(1.0, std::fmax(0.2, fac));

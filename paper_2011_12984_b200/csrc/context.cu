@@ -9,6 +9,7 @@
 
 #include <nccl.h>
 
+#include <chrono>
 #include <cstring>
 #include <thread>
 
@@ -317,4 +318,73 @@ extern "C" int SUNBW_ContextSetFakeComm(SUNBW_Context ctx, void* comm, int rank)
   delete ctx->comm;
   ctx->comm = c;
   return 0;
+}
+
+// ------------------------------------------------- launch-latency probe
+// Launch overhead dominates small problems (~8 us per kernel on
+// V100): the device time per back-to-back empty kernel launched eagerly, per
+// empty kernel node replayed from one CUDA graph, and the host round trip of
+// one launch + stream synchronisation.
+namespace {
+__global__ void k_empty() {}
+}  // namespace
+
+extern "C" int SUNBW_ProbeLaunchLatency(SUNBW_Context ctx, int64_t n, double* out3) {
+  if (!ctx || n < 1 || n > 10000000 || !out3) return SUNBW_ERR_ARG;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  int rc = 0;
+  float ms = 0.f;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    rc = SUNBW_ERR_CUDA;
+    goto done;
+  }
+  // (a) eager launches, device time per launch
+  for (int i = 0; i < 100; ++i) k_empty<<<1, 32, 0, s>>>();
+  cudaEventRecord(e0, s);
+  for (int64_t i = 0; i < n; ++i) k_empty<<<1, 32, 0, s>>>();
+  cudaEventRecord(e1, s);
+  if (cudaEventSynchronize(e1) != cudaSuccess) { rc = SUNBW_ERR_CUDA; goto done; }
+  cudaEventElapsedTime(&ms, e0, e1);
+  out3[0] = 1e3 * ms / (double)n;
+  {
+    // (b) one graph of min(n, 10000) kernel nodes, replayed until n nodes ran
+    const int64_t nodes = n < 10000 ? n : 10000, reps = (n + nodes - 1) / nodes;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { rc = SUNBW_ERR_CUDA; goto done; }
+    for (int64_t i = 0; i < nodes; ++i) k_empty<<<1, 32, 0, s>>>();
+    if (cudaStreamEndCapture(s, &g) != cudaSuccess || cudaGraphInstantiate(&ge, g, 0) != cudaSuccess ||
+        cudaGraphUpload(ge, s) != cudaSuccess || cudaGraphLaunch(ge, s) != cudaSuccess) {
+      rc = SUNBW_ERR_CUDA;
+      goto done;
+    }
+    cudaEventRecord(e0, s);
+    for (int64_t r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) { rc = SUNBW_ERR_CUDA; goto done; }
+    cudaEventElapsedTime(&ms, e0, e1);
+    out3[1] = 1e3 * ms / (double)(reps * nodes);
+  }
+  {
+    // (c) host round trip: launch + synchronise, mean over min(n, 2000)
+    const int64_t m = n < 2000 ? n : 2000;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < m; ++i) {
+      k_empty<<<1, 32, 0, s>>>();
+      cudaStreamSynchronize(s);
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    out3[2] = std::chrono::duration<double, std::micro>(t1 - t0).count() / (double)m;
+  }
+  ctx->launches += n + 100;
+done:
+  if (ge) cudaGraphExecDestroy(ge);
+  if (g) cudaGraphDestroy(g);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (s) cudaStreamDestroy(s);
+  if (cudaGetLastError() != cudaSuccess && !rc) rc = SUNBW_ERR_CUDA;
+  return rc ? ctx_set_err(ctx, rc) : 0;
 }

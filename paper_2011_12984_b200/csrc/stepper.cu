@@ -30,6 +30,8 @@
 #include <cstring>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "sunbw_internal.h"
 
 namespace sunbw {
@@ -44,7 +46,7 @@ int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, do
                  double rtol, double atol, const double* y, const double* fE, const double* hin,
                  double* hout, double* z, double* partials, unsigned long long* d_first,
                  int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end,
-                 const FusedFold* fold, int solver);
+                 const FusedFold* fold, int solver, bool tol);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
                double* d_min, double* d_nu, int* d_err);
 int fused_finalize_pending(SUNBW_Context ctx, double* pending, int K, int64_t nglobal, double* d_min,
@@ -53,7 +55,34 @@ int fused_finalize_pending(SUNBW_Context ctx, double* pending, int K, int64_t ng
 
 namespace {
 
+// local (singular, bad-ewt) flags as doubles, and back after the allreduce
+__global__ void k_flags(const unsigned long long* first, const int* err, double* flags) {
+  flags[0] = *first != ~0ull ? 1.0 : 0.0;
+  flags[1] = (err && *err) ? 1.0 : 0.0;
+}
+__global__ void k_flags_back(const double* flags, unsigned long long* first, int* err) {
+  if (flags[0] != 0.0 && *first == ~0ull) *first = 0;   // singular elsewhere: report block 0
+  if (err && flags[1] != 0.0) *err = 1;
+}
+
+}  // namespace
+
+int sunbw::or_flags_over_ranks(SUNBW_Context ctx, unsigned long long* d_first, int* d_err) {
+  if (ctx_nranks(ctx) <= 1) return 0;
+  double* flags = ctx->d_red + 96;
+  k_flags<<<1, 1, 0, ctx->stream>>>(d_first, d_err, flags);
+  ctx->launches++;
+  int e = ctx->comm->allreduce(flags, 2, RED_MAX, ctx->stream);
+  if (e) return ctx_set_err(ctx, e);
+  k_flags_back<<<1, 1, 0, ctx->stream>>>(flags, d_first, d_err);
+  ctx->launches++;
+  return ctx_check_launch(ctx);
+}
+
+namespace {
+
 constexpr int kMaxK = 32;
+constexpr int kMaxKF = 8;      // fused mode: K <= 8
 
 struct Stepper {
   void* prob;
@@ -69,6 +98,9 @@ struct Stepper {
   double* d_scal;        // [0] ewt min, [1..K] nu per iteration
   int* d_err;            // 1: non-positive ewt denominator seen
   double* d_partials;    // fused mode per-CTA partials
+  double* h_tol = nullptr;   // fused tolerance mode: pinned [min, nu_1..nu_8 | first | err]
+  int k_pred = 0;            // fused tolerance mode: the last step's iteration count
+  int64_t tol_launches = 0;  // fused tolerance mode: step launches (recomputations included)
   unsigned* d_counter = nullptr;   // fused mode: arrival counter of the in-kernel fold
   SUNLinearSolver gm = nullptr;   // linsol 1: SPGMR, block-LU preconditioner
   // fused mode on P > 1 ranks: halo on a side stream overlapping the
@@ -110,11 +142,26 @@ int alloc(Stepper* S, double** p, int64_t count) {
 }
 
 // ------------------------------------------------------------ timing hooks
+// NVTX range per stage, named by the paper's four timing categories
+// (advection incl. its communication, reaction, linear solve incl.
+// the Jacobian and matrix setup, and "other" = integrator + nonlinear solver
+// vector work); the fused kernel is all four in one launch.
+const char* nvtx_category(int kind) {
+  switch (kind) {
+    case BW_K_HALO: case BW_K_ADVECTION: return "advection (incl. halo)";
+    case BW_K_REACTION: return "reaction";
+    case BW_K_JACOBIAN: case BW_K_SCALEADDI: case BW_K_LU_SETUP: case BW_K_LU_SOLVE: return "linear solve";
+    case BW_K_FUSED_NEWTON: return "fused step (all categories)";
+    default: return "other";
+  }
+}
+
 struct Timed {
   Stepper* S;
   int kind;
   bool on;
   Timed(Stepper* s, int k) : S(s), kind(k), on(s->opt.timing != 0) {
+    nvtxRangePushA(nvtx_category(k));
     if (!on) return;
     if (S->ev_used + 2 > S->ev_pool.size()) {
       for (int i = 0; i < 64; ++i) {
@@ -127,6 +174,7 @@ struct Timed {
                              S->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
   ~Timed() {
+    nvtxRangePop();
     if (!on) return;
     cudaEventRecordWithFlags(S->ev_pool[S->ev_used + 1], S->ctx->stream,
                              S->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
@@ -193,46 +241,97 @@ int enqueue_step(Stepper* S, bool first) {
   }
 
   if (o.fused) {
-    int nb = 0, nb2 = 0;
     const int solver = o.numerics == 1 ? 2 : (o.linsol == 2 ? 1 : 0);
     // partials are folded by the step's last CTA unless a blocking
     // allreduce must sit between fold and finalisation (P > 1, not deferred)
     const bool fold_in_kernel = S->deferred || ctx_nranks(ctx) <= 1;
-    sunbw::FusedFold fold{0, S->d_counter, S->deferred ? S->d_pending : nullptr, S->d_scal, S->d_scal + 1,
-                          S->d_err, S->nglobal};
-    const sunbw::FusedFold* fk = fold_in_kernel ? &fold : nullptr;
-    if (split) {
-      const int64_t tpp = fa.nx * fa.ny / 128;          // tiles per z-plane
-      if (cudaEventRecord(S->evA, ctx->stream) != cudaSuccess ||
-          cudaStreamWaitEvent(S->side, S->evA, 0) != cudaSuccess)
+    // one launch sequence of the step with Kr Newton iterations (tolk: the
+    // tolerance-mode kernel, every iteration's nu); with_halo: the P > 1
+    // split around the side-stream halo (a recomputation reuses the halo)
+    auto run = [&](int Kr, bool tolk, bool with_halo) -> int {
+      int nb = 0, nb2 = 0;
+      sunbw::FusedFold fold{0, S->d_counter, S->deferred ? S->d_pending : nullptr, S->d_scal, S->d_scal + 1,
+                            S->d_err, S->nglobal};
+      const sunbw::FusedFold* fk = fold_in_kernel ? &fold : nullptr;
+      if (split && with_halo) {
+        const int64_t tpp = fa.nx * fa.ny / 128;          // tiles per z-plane
+        if (cudaEventRecord(S->evA, ctx->stream) != cudaSuccess ||
+            cudaStreamWaitEvent(S->side, S->evA, 0) != cudaSuccess)
+          return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+        TRY(sunbw::bw_halo_stream(S->prob, y, S->side));
+        if (cudaEventRecord(S->evB, S->side) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+        {
+          Timed t(S, BW_K_FUSED_NEWTON);
+          TRY(sunbw::fused_newton(ctx, S->prob, G, first, Kr, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
+                                  S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr, solver, tolk));
+        }
+        if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+        fold.prev_parts = nb;
+        {
+          Timed t(S, BW_K_FUSED_NEWTON);
+          TRY(sunbw::fused_newton(ctx, S->prob, G, first, Kr, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
+                                  S->d_partials + (int64_t)nb * (Kr + 1), S->d_first, &nb2, &fa, 0, tpp,
+                                  fk, solver, tolk));
+        }
+      } else {
+        Timed t(S, BW_K_FUSED_NEWTON);
+        TRY(sunbw::fused_newton(ctx, S->prob, G, first, Kr, h, o.rtol, o.atol, y,
+                                adv_in_kernel ? nullptr : fE_n, fEp, fE, z, S->d_partials, S->d_first, &nb,
+                                adv_in_kernel ? &fa : nullptr, 0, -1, fk, solver, tolk));
+      }
+      if (!fold_in_kernel) {
+        Timed t(S, BW_K_WRMS);
+        TRY(sunbw::fused_fold(ctx, S->d_partials, nb + nb2, Kr, S->nglobal, S->d_scal, S->d_scal + 1,
+                              S->d_err));
+      }
+      return 0;
+    };
+    if (o.newton_mode != 1) return run(o.K, false, true);
+
+    // Tolerance mode, fused (DESIGN R31): the step kernel runs a
+    // predicted number of iterations Kr (the last step's count) and reports
+    // every iteration's global nu; the host takes the oracle's decision --
+    // the first k with nu_k <= tol_nl -- and recomputes the step (its inputs
+    // are untouched) when that k differs from Kr: with k if k < Kr, with the
+    // maximum K if none of the Kr converged.  No convergence within K:
+    // recoverable failure, as on the composed path.
+    int Kr = S->k_pred > 0 && S->k_pred <= o.K ? S->k_pred : o.K;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      TRY(run(Kr, true, attempt == 0));
+      TRY(sunbw::or_flags_over_ranks(ctx, S->d_first, S->d_err));
+      if (cudaMemcpyAsync(S->h_tol, S->d_scal, sizeof(double) * (Kr + 1), cudaMemcpyDeviceToHost,
+                          ctx->stream) != cudaSuccess ||
+          cudaMemcpyAsync(S->h_tol + kMaxKF + 1, S->d_first, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ctx->stream) != cudaSuccess ||
+          cudaMemcpyAsync(S->h_tol + kMaxKF + 2, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) !=
+              cudaSuccess ||
+          cudaStreamSynchronize(ctx->stream) != cudaSuccess)
         return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-      TRY(sunbw::bw_halo_stream(S->prob, y, S->side));
-      if (cudaEventRecord(S->evB, S->side) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-      {
-        Timed t(S, BW_K_FUSED_NEWTON);
-        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
-                                S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr, solver));
+      S->tol_launches++;
+      if (attempt > 0) S->st.setups++;   // a recomputation repeats the Setup (stats: setups per launch)
+      const unsigned long long f = *(const unsigned long long*)(S->h_tol + kMaxKF + 1);
+      if (*(const int*)(S->h_tol + kMaxKF + 2)) return SUNBW_RECOV_BAD_EWT;
+      if (f != ~0ull) { S->st.singular = (int64_t)f; return SUNBW_RECOV_SINGULAR; }
+      int kstar = 0;
+      for (int k = 1; k <= Kr && !kstar; ++k)
+        if (S->h_tol[k] <= o.tol_nl) kstar = k;            // same global nu on every rank (R17)
+      if (kstar == Kr) {
+        S->st.newton_iters += Kr;
+        S->st.last_nu = S->h_tol[Kr];
+        S->k_pred = Kr;
+        return 0;
       }
-      if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-      fold.prev_parts = nb;
-      {
-        Timed t(S, BW_K_FUSED_NEWTON);
-        TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
-                                S->d_partials + (int64_t)nb * (o.K + 1), S->d_first, &nb2, &fa, 0, tpp,
-                                fk, solver));
+      if (kstar > 0) {
+        Kr = kstar;                  // converged earlier than predicted: redo with exactly kstar
+      } else if (Kr == o.K) {
+        S->st.newton_iters += o.K;
+        S->st.last_nu = S->h_tol[o.K];
+        return SUNBW_RECOV_NONCONV;
+      } else {
+        Kr = o.K;                    // not converged within Kr: redo with the maximum
       }
-    } else {
-      Timed t(S, BW_K_FUSED_NEWTON);
-      TRY(sunbw::fused_newton(ctx, S->prob, G, first, o.K, h, o.rtol, o.atol, y,
-                              adv_in_kernel ? nullptr : fE_n, fEp, fE, z, S->d_partials, S->d_first, &nb,
-                              adv_in_kernel ? &fa : nullptr, 0, -1, fk, solver));
     }
-    if (!fold_in_kernel) {
-      Timed t(S, BW_K_WRMS);
-      TRY(sunbw::fused_fold(ctx, S->d_partials, nb + nb2, o.K, S->nglobal, S->d_scal, S->d_scal + 1,
-                            S->d_err));
-    }
-    return 0;
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);   // unreachable: at most Kr -> K -> kstar
   }
 
   {
@@ -271,7 +370,9 @@ int enqueue_step(Stepper* S, bool first) {
 
   const bool tol = o.newton_mode == 1;
   if (tol) {
-    // the host needs the singular flag and the ewt check before iterating
+    // the host needs the singular flag and the ewt check before iterating;
+    // every rank must take the same branch (the collectives below pair up)
+    TRY(sunbw::or_flags_over_ranks(ctx, S->d_first, S->d_err));
     unsigned long long f = 0;
     int err = 0;
     if (cudaMemcpyAsync(&f, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
@@ -317,16 +418,6 @@ int enqueue_step(Stepper* S, bool first) {
     }
   }
   return tol ? SUNBW_RECOV_NONCONV : 0;
-}
-
-// local (singular, bad-ewt) flags as doubles, and back after the allreduce
-__global__ void k_flags(const unsigned long long* first, const int* err, double* flags) {
-  flags[0] = *first != ~0ull ? 1.0 : 0.0;
-  flags[1] = *err ? 1.0 : 0.0;
-}
-__global__ void k_flags_back(const double* flags, unsigned long long* first, int* err) {
-  if (flags[0] != 0.0 && *first == ~0ull) *first = 0;   // singular elsewhere: report block 0
-  if (flags[1] != 0.0) *err = 1;
 }
 
 void rotate(Stepper* S) {
@@ -401,6 +492,26 @@ int capture_step(Stepper* S, int key) {
   return 0;
 }
 
+// Captures (and uploads) the step graph of every rotation state (3 state
+// buffers x 2 history buffers = 6 keys, the rotation's period) at the first
+// graph step, so that no capture or first-launch upload lands inside a later
+// Advance call (a timed region).
+int capture_all_keys(Stepper* S) {
+  const int iy = S->iy, iyp = S->iyp, iz = S->iz, ife = S->ife, ifep = S->ifep;
+  int rc = 0;
+  for (int r = 0; r < 6 && !rc; ++r) {
+    const int key = graph_key(S);
+    if (!S->gexec[key]) {
+      rc = capture_step(S, key);
+      if (!rc && cudaGraphUpload(S->gexec[key], S->ctx->stream) != cudaSuccess)
+        rc = ctx_set_err(S->ctx, SUNBW_ERR_CUDA);
+    }
+    rotate(S);
+  }
+  S->iy = iy; S->iyp = iyp; S->iz = iz; S->ife = ife; S->ifep = ifep;
+  return rc;
+}
+
 }  // namespace
 
 // ==================================================================== C ABI
@@ -412,7 +523,9 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   if (opt->linsol < 0 || opt->linsol > 2 || (opt->linsol == 1 && (opt->maxl < 1 || opt->maxl > 60)))
     return SUNBW_ERR_ARG;
   if (opt->numerics < 0 || opt->numerics > 1) return SUNBW_ERR_ARG;
-  if (opt->fused && (opt->newton_mode != 0 || opt->K > 8 || opt->linsol == 1)) return SUNBW_ERR_UNSUPPORTED;
+  if (opt->fused && (opt->K > 8 || opt->linsol == 1)) return SUNBW_ERR_UNSUPPORTED;
+  // fused tolerance mode: the contracted cell step (R30, R31)
+  if (opt->fused && opt->newton_mode == 1 && opt->numerics != 1) return SUNBW_ERR_UNSUPPORTED;
   if (opt->fused && opt->numerics == 1 && opt->linsol != 0) return SUNBW_ERR_UNSUPPORTED;
   SUNBW_Context ctx = y0->ctx;
   int64_t G = sunbw::bw_local_cells(prob);
@@ -459,6 +572,9 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   if (!e && cudaMalloc(&S->d_first, sizeof(unsigned long long)) != cudaSuccess) e = SUNBW_ERR_MEM;
   if (!e && cudaMalloc(&S->d_err, sizeof(int)) != cudaSuccess) e = SUNBW_ERR_MEM;
   if (!e && cudaMalloc(&S->d_counter, sizeof(unsigned)) != cudaSuccess) e = SUNBW_ERR_MEM;
+  if (!e && opt->fused && opt->newton_mode == 1 &&
+      cudaHostAlloc(&S->h_tol, sizeof(double) * (kMaxKF + 4), cudaHostAllocDefault) != cudaSuccess)
+    e = SUNBW_ERR_MEM;
   if (e) {
     cudaGetLastError();
     BW_StepperDestroy(S);
@@ -507,7 +623,7 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
     if (S->opt.use_graph && !first) {
       int key = graph_key(S);
       if (!S->gexec[key]) {
-        int e = capture_step(S, key);
+        int e = capture_all_keys(S);
         if (e) return e;
       }
       if (S->opt.timing && !S->ev_nodes[key].empty()) {
@@ -533,7 +649,7 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
     } else {
       int64_t it0 = S->st.newton_iters;
       rc = enqueue_step(S, first);
-      if (S->opt.fused) S->st.newton_iters = it0 + S->opt.K;
+      if (S->opt.fused && S->opt.newton_mode == 0) S->st.newton_iters = it0 + S->opt.K;
       if (rc < 0) return rc;
       if (rc > 0) { S->st.fails++; break; }
     }
@@ -554,13 +670,7 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
   }
   if (S->opt.newton_mode == 0 && ctx_nranks(ctx) > 1) {
     // every rank returns the same code: OR the local flags over the ranks
-    double* flags = ctx->d_red + 96;
-    k_flags<<<1, 1, 0, ctx->stream>>>(S->d_first, S->d_err, flags);
-    ctx->launches++;
-    int e = ctx->comm->allreduce(flags, 2, RED_MAX, ctx->stream);
-    if (e) return ctx_set_err(ctx, e);
-    k_flags_back<<<1, 1, 0, ctx->stream>>>(flags, S->d_first, S->d_err);
-    ctx->launches++;
+    TRY(sunbw::or_flags_over_ranks(ctx, S->d_first, S->d_err));
   }
   if (S->opt.newton_mode == 0) {
     if (cudaMemcpyAsync(&f, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
@@ -572,7 +682,9 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
       cudaMemcpyAsync(y_out->d, S->y[S->iy], sizeof(double) * S->n, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-  if (S->opt.timing) harvest_timing(S);
+  // timing events are read lazily (BW_StepperKernelTimes, or the next call
+  // once many are pending): no host work after the step kernels here
+  if (S->opt.timing && S->ev_used > 4096) harvest_timing(S);
   if (S->opt.newton_mode == 0 && nsteps > 0) {
     S->st.last_nu = nu;
     if (f != ~0ull) { S->st.singular = (int64_t)f; rc = rc ? rc : SUNBW_RECOV_SINGULAR; }
@@ -603,6 +715,10 @@ extern "C" int BW_StepperReset(void* stepper, N_Vector y0, double t0) {
 extern "C" int BW_StepperKernelTimes(void* stepper, double* ms, int64_t* launches, int reset) {
   auto* S = (Stepper*)stepper;
   if (!S) return SUNBW_ERR_ARG;
+  if (S->opt.timing && !S->ev_kind.empty()) {
+    if (cudaStreamSynchronize(S->ctx->stream) != cudaSuccess) return ctx_set_err(S->ctx, SUNBW_ERR_CUDA);
+    harvest_timing(S);
+  }
   for (int k = 0; k < BW_K_COUNT_; ++k) {
     if (ms) ms[k] = S->k_ms[k];
     if (launches) launches[k] = S->k_count[k];
@@ -634,6 +750,7 @@ extern "C" int BW_StepperDestroy(void* stepper) {
   if (S->evA) cudaEventDestroy(S->evA);
   if (S->evB) cudaEventDestroy(S->evB);
   if (S->d_pending) cudaFree(S->d_pending);
+  if (S->h_tol) cudaFreeHost(S->h_tol);
   delete S;
   return 0;
 }

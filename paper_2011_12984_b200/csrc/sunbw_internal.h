@@ -182,6 +182,12 @@ int fused_multistep(SUNBW_Context ctx, void* prob, const SmallGeom& gm, int64_t 
                     double* y_out, double* hout, double* d_scal, int* d_err, unsigned long long* d_first,
                     int64_t nglobal);
 
+// OR the local recoverable-failure flags over the ranks (the ensemble
+// of task-local solves succeeds or fails as one): afterwards *d_first is
+// unchanged, or 0 if a singular block was flagged only on another rank, and
+// *d_err (may be nullptr) is 1 if any rank set it.  No-op on one rank.
+int or_flags_over_ranks(SUNBW_Context ctx, unsigned long long* d_first, int* d_err);
+
 struct FusedFold {
   int prev_parts;            // partial rows written by earlier launches of this step
   unsigned* counter;         // zero-initialised

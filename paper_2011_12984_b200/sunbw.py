@@ -87,6 +87,7 @@ _SIGS = {
     "SUNBW_ContextRank": (_I, [_P]),
     "SUNBW_ContextNRanks": (_I, [_P]),
     "SUNBW_SelfTestDivision": (_I, [_P, _I64, _P, _P, _P]),
+    "SUNBW_ProbeLaunchLatency": (_I, [_P, _I64, _P]),
     "N_VNew_B200": (_P, [_P, _I64]),
     "N_VMake_B200": (_P, [_P, _I64, _P]),
     "N_VClone": (_P, [_P]),
@@ -244,6 +245,13 @@ def selftest_division(ctx: "Context", a: torch.Tensor, b: torch.Tensor):
     out = (_I64 * 2)()
     _check(lib().SUNBW_SelfTestDivision(ctx.handle, a.numel(), _P(a.data_ptr()), _P(b.data_ptr()), out),
            "SUNBW_SelfTestDivision")
+    return tuple(out)
+
+
+def probe_launch_latency(ctx: "Context", n: int = 100_000):
+    """(eager us/launch, graph us/node, host launch+sync round trip us)."""
+    out = (C.c_double * 3)()
+    _check(lib().SUNBW_ProbeLaunchLatency(ctx.handle, n, out), "SUNBW_ProbeLaunchLatency")
     return tuple(out)
 
 

@@ -1,0 +1,12 @@
+# evidence run: tests, ncu (summaries only come back; reports deleted), bench
+set -x
+timeout 900 python -m pytest tests/test_gpu_fused_tol.py tests/test_gpu_multirank_flags.py -q -p no:cacheprovider > gpurun_out/pytest_tol.log 2>&1; tail -3 gpurun_out/pytest_tol.log
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:fused_newton -s 3 -c 1 -o /tmp/prof_ct python bench.py --steps 5 --warmup 3 --no-ops --no-cpu > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:fused_newton -s 3 -c 1 -o /tmp/prof_ex python bench.py --steps 5 --warmup 3 --no-ops --no-cpu --numerics exact > /dev/null 2>&1
+python tools/traffic_json.py /tmp/prof_ct.ncu-rep /tmp/prof_ex.ncu-rep > /dev/null 2>&1; cp profiles/ncu_traffic.json gpurun_out/
+python tools/ncu_summary.py /tmp/prof_ct.ncu-rep > gpurun_out/ncu_summary_ct.txt; python tools/ncu_summary.py /tmp/prof_ex.ncu-rep > gpurun_out/ncu_summary_ex.txt
+python tools/ncu_stalls.py /tmp/prof_ct.ncu-rep > gpurun_out/ncu_stalls_ct.txt 2>&1
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 300 gpurun_out/bench_default.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_fused.csv python bench.py --steps 5 --warmup 3 --no-ops --no-cpu > /dev/null 2>&1
+timeout 300 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2>&1; tail -c 300 gpurun_out/bench_ref.json
+du -sh gpurun_out
