@@ -67,6 +67,7 @@ struct Ark {
   unsigned long long* d_first;
   double t = 0.0, h = 0.0;
   BW_ArkStats st{};
+  sunbw::ArkFused* fused = nullptr;   // opt.fused: one kernel per stage (ark_fused.cu, R32)
 };
 
 double host_wrms(SUNBW_Context ctx, int64_t n, int64_t nglob, const double* x, const double* w, int* e) {
@@ -178,7 +179,9 @@ int attempt(Ark* A, int* nl_ok, double* dsm) {
 extern "C" int BW_ArkCreate(void* prob, N_Vector y0, const BW_ArkOptions* opt, void** out) {
   if (!prob || !y0 || !opt || !out) return SUNBW_ERR_ARG;
   *out = nullptr;
-  if (!(opt->h0 > 0) || opt->maxnl < 1 || opt->max_steps < 1) return SUNBW_ERR_ARG;
+  if (!(opt->h0 > 0) || opt->maxnl < 1 || opt->max_steps < 1 || (opt->fused != 0 && opt->fused != 1))
+    return SUNBW_ERR_ARG;
+  if (opt->fused && opt->maxnl > 4) return SUNBW_ERR_UNSUPPORTED;   // fused stages: maxnl <= 4
   SUNBW_Context ctx = y0->ctx;
   int64_t G = sunbw::bw_local_cells(prob);
   if (y0->local_len != 3 * G) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
@@ -199,6 +202,7 @@ extern "C" int BW_ArkCreate(void* prob, N_Vector y0, const BW_ArkOptions* opt, v
   ok = ok && cudaMalloc(&A->M, sizeof(double) * 9 * (G > 0 ? G : 1)) == cudaSuccess &&
        cudaMalloc(&A->piv, sizeof(int32_t) * (G > 0 ? G : 1)) == cudaSuccess &&
        cudaMalloc(&A->d_first, sizeof(unsigned long long)) == cudaSuccess;
+  if (ok && opt->fused) ok = (A->fused = sunbw::ark_fused_create(ctx, prob, A->nglobal)) != nullptr;
   if (!ok ||
       cudaMemcpyAsync(A->y, y0->d, sizeof(double) * A->n, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess) {
     cudaGetLastError();
@@ -226,7 +230,10 @@ extern "C" int BW_ArkEvolve(void* ark, double t_end, N_Vector y_out, BW_ArkStats
     if (A->h < 1e-14 * (1.0 + A->t)) { rc = 2; break; }
     int nl_ok = 1;
     double dsm = 0.0;
-    int e = attempt(A, &nl_ok, &dsm);
+    int e = A->fused ? sunbw::ark_fused_attempt(A->fused, A->y, A->ynew, A->h, A->opt.rtol, A->opt.atol,
+                                                A->opt.tol_nl, A->opt.maxnl, &nl_ok, &dsm,
+                                                &A->st.newton_iters, &A->st.setups)
+                     : attempt(A, &nl_ok, &dsm);
     if (e < 0) return e;
     if (!nl_ok) {
       A->st.rejected_nl++;
@@ -266,6 +273,7 @@ extern "C" int BW_ArkDestroy(void* ark) {
     if (b) cudaFree(b);
   if (A->piv) cudaFree(A->piv);
   if (A->d_first) cudaFree(A->d_first);
+  sunbw::ark_fused_destroy(A->fused);
   delete A;
   return 0;
 }

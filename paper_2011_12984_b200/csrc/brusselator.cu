@@ -455,6 +455,24 @@ bool bw_small_geometry(void* prob, SmallGeom* g) {
   return true;
 }
 
+void bw_ark_geometry(void* prob, ArkGeometry* g) {
+  auto* P = (Prob*)prob;
+  const BW_BrussParams& p = P->p;
+  g->dim = p.dim;
+  g->expl = p.reaction_only ? 2 : (p.kind == 1 ? 1 : 0);
+  g->has_y = p.ny > 1;
+  g->has_z = p.nz > 1;
+  g->nx = P->nxl;
+  g->ny = P->nyl;
+  g->nzl = P->nzl;
+  g->G = P->G;
+  g->halo_len = P->halo_len;
+  g->kx = P->kx;
+  g->ky = P->ky;
+  g->kz = P->kz;
+  g->lam_E = p.lam_E;
+}
+
 bool bw_fused_advection(void* prob, const double* y, FusedAdvection* fa) {
   auto* P = (Prob*)prob;
   const BW_BrussParams& p = P->p;

@@ -188,6 +188,23 @@ int fused_multistep(SUNBW_Context ctx, void* prob, const SmallGeom& gm, int64_t 
 // *d_err (may be nullptr) is 1 if any rank set it.  No-op on one rank.
 int or_flags_over_ranks(SUNBW_Context ctx, unsigned long long* d_first, int* d_err);
 
+// Geometry and explicit operator of a problem for the fused ARK stage
+// kernels (ark_fused.cu): local extents, which axes carry an advection term,
+// and the explicit operator kind (0 upwind advection, 1 f_E = λ_E y, 2 f_E = 0)
+struct ArkGeometry {
+  int dim, expl, has_y, has_z;
+  int64_t nx, ny, nzl, G, halo_len;
+  double kx, ky, kz, lam_E;
+};
+void bw_ark_geometry(void* prob, ArkGeometry* g);
+// one attempted ARK step on the device (ark_fused.cu); see the definition
+struct ArkFused;
+ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal);
+void ark_fused_destroy(ArkFused* F);
+int ark_fused_attempt(ArkFused* F, const double* y, double* ynew, double h, double rtol, double atol,
+                      double tol_nl, int maxnl, int* nl_ok, double* dsm, int64_t* newton_iters,
+                      int64_t* setups);
+
 struct FusedFold {
   int prev_parts;            // partial rows written by earlier launches of this step
   unsigned* counter;         // zero-initialised

@@ -610,8 +610,8 @@ class Ark:
     """Adaptive IMEX ARK3(2)4L[2]SA integrator (BW_ArkCreate / BW_ArkEvolve)."""
 
     def __init__(self, P: Problem, y0: NVector, h0=1e-4, rtol=1e-6, atol=1e-9, tol_nl=0.1, maxnl=3,
-                 max_steps=100000, fixed=False):
-        self.opts = BW_ArkOptions(h0, rtol, atol, tol_nl, maxnl, max_steps, int(bool(fixed)), 0)
+                 max_steps=100000, fixed=False, fused=False):
+        self.opts = BW_ArkOptions(h0, rtol, atol, tol_nl, maxnl, max_steps, int(bool(fixed)), int(bool(fused)))
         h = _P()
         _check(lib().BW_ArkCreate(P, y0, C.byref(self.opts), C.byref(h)), "BW_ArkCreate")
         self.handle = h.value

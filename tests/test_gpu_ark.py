@@ -40,39 +40,89 @@ def rel(a, b):
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0)))
 
 
-def test_ark_C1_brusselator(S, ctx):
+@pytest.mark.parametrize("fused", [False, True])
+def test_ark_C1_brusselator(S, ctx, fused):
     nx = 64
     y0 = oracle.bruss_ic(nx)
     rc2, yref, st2 = oracle.ark_integrate(y0, 1.0, h0=1e-4, nx=nx, kx=0.01 * nx)
-    rc, y, st = run(S, ctx, S.bruss_params(dim=1, nx=nx), y0, 1.0, h0=1e-4)
+    rc, y, st = run(S, ctx, S.bruss_params(dim=1, nx=nx), y0, 1.0, h0=1e-4, fused=fused)
     assert rc == rc2 == 0
     for k in ("accepted", "rejected_err", "rejected_nl", "newton_iters", "setups"):
         assert st[k] == st2[k], k
     assert rel(y, yref) <= 1e-9
 
 
-def test_ark_fixed_step_linear(S, ctx):
+@pytest.mark.parametrize("fused", [False, True])
+def test_ark_fixed_step_linear(S, ctx, fused):
     G = 999
     y0 = np.linspace(0.5, 1.5, 3 * G)
     params = S.bruss_params(dim=1, nx=G, kind=1, lam_E=-1.0, lam_I=-10.0)
-    rc2, yref, _ = oracle.ark_integrate(y0, 1.0, h0=1.0 / 80, fixed=True, kind=1, nx=G, lam_E=-1.0,
-                                        lam_I=-10.0, maxnl=4, tol_nl=1e-4)
-    rc, y, st = run(S, ctx, params, y0, 1.0, h0=1.0 / 80, fixed=True, maxnl=4, tol_nl=1e-4)
-    assert rc == rc2 == 0 and st["accepted"] == 80
-    assert rel(y, yref) <= 1e-12
+    rc2, yref, st2 = oracle.ark_integrate(y0, 1.0, h0=1.0 / 80, fixed=True, kind=1, nx=G, lam_E=-1.0,
+                                          lam_I=-10.0, maxnl=4, tol_nl=1e-4)
+    rc, y, st = run(S, ctx, params, y0, 1.0, h0=1.0 / 80, fixed=True, maxnl=4, tol_nl=1e-4, fused=fused)
+    assert rc == rc2 == 0 and st["accepted"] == 80 and st["newton_iters"] == st2["newton_iters"]
+    assert rel(y, yref) <= (1e-11 if fused else 1e-12)
 
 
-def test_ark_3D_and_retries(S, ctx):
+@pytest.mark.parametrize("fused", [False, True])
+def test_ark_3D_and_retries(S, ctx, fused):
     nx, ny, nz = 12, 10, 8
     y0 = oracle.bruss_ic(nx, ny, nz)
     kx = 0.01 * nx
     rc2, yref, st2 = oracle.ark_integrate(y0, 0.05, h0=1e-4, nx=nx, ny=ny, nz=nz, kx=kx, ky=0.01 * ny,
                                           kz=0.01 * nz)
-    rc, y, st = run(S, ctx, S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz), y0, 0.05, h0=1e-4)
-    assert rc == rc2 == 0 and st["accepted"] == st2["accepted"]
+    rc, y, st = run(S, ctx, S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz), y0, 0.05, h0=1e-4, fused=fused)
+    assert rc == rc2 == 0
+    for k in ("accepted", "rejected_err", "rejected_nl", "newton_iters", "setups"):
+        assert st[k] == st2[k], k
     assert rel(y, yref) <= 1e-9
     # one Newton iteration per stage with an unreachable tolerance: every
     # attempt fails and the step is recomputed with h/4 until max_steps
     rc, _, st = run(S, ctx, S.bruss_params(dim=1, nx=64), oracle.bruss_ic(64), 0.01, h0=1e-3,
-                    maxnl=1, tol_nl=1e-300, max_steps=5)
+                    maxnl=1, tol_nl=1e-300, max_steps=5, fused=fused)
     assert rc == 1 and st["rejected_nl"] == 5 and st["accepted"] == 0
+
+
+def test_ark_fused_C3_shape(S, ctx):
+    """The bench's ARK row: C3-shaped grid (reduced to 64^3 here for the
+    oracle's time) to t = 0.003, fused stages vs the oracle."""
+    n = 64
+    y0 = oracle.bruss_ic(n, n, n)
+    k = 0.01 * n
+    rc2, yref, st2 = oracle.ark_integrate(y0, 0.003, h0=1e-4, nx=n, ny=n, nz=n, kx=k, ky=k, kz=k)
+    rc, y, st = run(S, ctx, S.bruss_params(dim=3, nx=n, ny=n, nz=n), y0, 0.003, h0=1e-4, fused=True)
+    assert rc == rc2 == 0
+    for key in ("accepted", "rejected_err", "rejected_nl", "newton_iters", "setups"):
+        assert st[key] == st2[key], key
+    assert rel(y, yref) <= 1e-9
+
+
+def test_ark_fused_multirank(S):
+    """P = 2 logical ranks (fake communicator): the stage halos and the
+    per-attempt allreduce of all stage norms; same counts and state as the
+    one-rank oracle run."""
+    from test_gpu_bruss import run_ranks
+    nx, ny, nz = 12, 10, 8
+    y0 = oracle.bruss_ic(nx, ny, nz)
+    params = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz)
+    rc2, yref, st2 = oracle.ark_integrate(y0, 0.02, h0=1e-4, nx=nx, ny=ny, nz=nz, kx=0.01 * nx,
+                                          ky=0.01 * ny, kz=0.01 * nz)
+
+    def fn(c, r):
+        P = S.Problem(c, params)
+        n, off = 3 * P.local_cells, 3 * P.cell_offset
+        yd = torch.from_numpy(y0[off:off + n].copy()).cuda()
+        yout = torch.empty_like(yd)
+        A = S.Ark(P, S.NVector(c, yd), h0=1e-4, fused=True)
+        rc, st = A.evolve(0.02, S.NVector(c, yout))
+        c.stream.synchronize()
+        res = (rc, off, yout.cpu().numpy(), st)
+        A.destroy(); P.destroy()
+        return res
+
+    res = run_ranks(S, 2, fn)
+    assert all(r[0] == 0 for r in res)
+    for key in ("accepted", "rejected_err", "rejected_nl", "newton_iters"):
+        assert res[0][3][key] == res[1][3][key] == st2[key], key
+    y = np.concatenate([r[2] for r in sorted(res, key=lambda t: t[1])])
+    assert rel(y, yref) <= 1e-9
