@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 BYTES_PER_CELL = {
     "advection": 48, "rhs_combine": 120, "ewt": 216, "predict": 48, "jacobian": 96,
     "scaleaddi": 144, "lu_setup": 148, "reaction": 48, "residual": 96, "lu_solve": 124,
-    "update": 72, "wrms": 48, "fused_newton": 96, "halo": 0,
+    "update": 72, "wrms": 48, "fused_newton": 96, "halo": 0, "fused_plane0": 96,
 }
 WRMS_FUSED_BYTES = 0        # the fused path's fold reads only per-CTA partials
 NUM_SMS = 148
@@ -637,12 +637,20 @@ def main():
     peak, peak_kind = measured_peak()
     kt = st.kernel_times(reset=True)
     kernels = {}
+    plane = n_ax * n_ax
     for name, (kms, cnt) in kt.items():
         bpc = BYTES_PER_CELL.get(name, 0)
         if fused and name == "wrms":
             bpc = WRMS_FUSED_BYTES
+        # cells per launch: at N > 1 the fused step is split into the interior
+        # planes (fused_newton) and plane 0 after the halo (fused_plane0)
+        cells = G
+        if fused and world > 1 and name == "fused_newton":
+            cells = G - plane
+        elif name == "fused_plane0":
+            cells = plane
         avg = kms / cnt
-        ach = bpc * G / (avg * 1e-3) / 1e9 if bpc else 0.0
+        ach = bpc * cells / (avg * 1e-3) / 1e9 if bpc else 0.0
         kernels[name] = {"ms_total": round(kms, 3), "launches": cnt, "us_avg": round(avg * 1e3, 2),
                          "share": round(kms / ms_local, 4), "GB/s": round(ach, 1)}
     dom = max(kernels, key=lambda k: kernels[k]["ms_total"] if BYTES_PER_CELL.get(k) else -1)
@@ -655,7 +663,8 @@ def main():
                                   + (f", {ent['source']}" if ent else ""),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                 else "fallback (B200_PROFILING.md)",
-                "bytes_per_launch": BYTES_PER_CELL[dom] * G,
+                "bytes_per_launch": BYTES_PER_CELL[dom] * (G - plane if (fused and world > 1 and dom == "fused_newton")
+                                                           else G),
                 "bytes_per_unit": {"unit": "cell", "bytes": BYTES_PER_CELL[dom]}}
     if ent and ent.get("fp64_per_cell"):
         # the fused step is as much an fp64-ALU kernel as an HBM one
@@ -668,6 +677,17 @@ def main():
                             "frac": round(a64 / p64, 4), "ops_per_cell": ops,
                             "peak_source": "148 SMs x 64 FP64 lanes/clk (profiles/r01d_fp64_latency.txt: "
                                            "0.49 fp64 warp-instr/clk/SMSP) x sm_max_mhz"}
+    # P > 1, fused: the copy-engine halo (side stream) against the interior
+    # launch it overlaps
+    overlap = None
+    if fused and world > 1 and "halo" in kernels and "fused_plane0" in kernels:
+        hu, iu, pu = (kernels[k]["us_avg"] for k in ("halo", "fused_newton", "fused_plane0"))
+        su = 1e3 * ms / args.steps
+        overlap = {"halo_us": hu, "interior_us": iu, "plane0_us": pu, "step_us": round(su, 2),
+                   "exposed_us": round(su - iu - pu, 2),
+                   "halo_hidden": bool(su - iu - pu < hu),
+                   "mechanism": "copy engine (peer_halo.cu)" if os.environ.get("SUNBW_PEER_HALO", "1") != "0"
+                   else "NCCL send/recv"}
     # bytes per step of this mode; the composed path's are SURVEY §8(d)'s
     # 820 + 388 K per cell, the fused step's 96 per cell (R28)
     step_bytes = sum(BYTES_PER_CELL[k] * G * v["launches"] for k, v in kernels.items()
@@ -728,7 +748,7 @@ def main():
             "step_GB/s": round(step_bytes / (ms / args.steps * 1e-3) / 1e9, 1),
             "kernels": kernels, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "cpu_baseline": cpu, "nvector_ops_1e8": ops, "nvector_ops_1e9": ops_1e9,
-            "launch_latency": latency, "other_configs": configs,
+            "launch_latency": latency, "other_configs": configs, "halo_overlap": overlap,
             "newton_iters": stats["newton_iters"],
         }
         print(json.dumps(line), flush=True)

@@ -15,7 +15,7 @@ OBJDIR = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libsunbw.so")
 
 SOURCES = ["context.cu", "nvector.cu", "blockdiag.cu", "brusselator.cu", "stepper.cu", "fused.cu",
-           "gmres.cu", "ark.cu", "ark_fused.cu", "vecarray.cu"]
+           "gmres.cu", "ark.cu", "ark_fused.cu", "vecarray.cu", "peer_halo.cu"]
 HEADERS = ["sunbw_internal.h", "sunbw_device.cuh", "pipeline.cuh", "cellstep.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -32,6 +32,7 @@
 // step / iteration counts (tests/test_gpu_ark.py).
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "sunbw_internal.h"
@@ -85,32 +86,6 @@ struct Args {
   unsigned long long* first;    // first singular cell (1-based), this stage
   int krt;                      // Newton iterations of this launch
 };
-
-// f_E of state Zj at cell c = (i, jy, k): upwind stencil (O9 terms, contracted)
-__device__ __forceinline__ void explicit_rhs(const Geom& g, const double* Zj, const double* bj, int64_t c,
-                                             int64_t i, int64_t jy, int64_t k, const double (&q)[3],
-                                             double (&fe)[3]) {
-  if (g.expl == 2) {
-    fe[0] = fe[1] = fe[2] = 0.0;
-    return;
-  }
-  if (g.expl == 1) {
-#pragma unroll
-    for (int s = 0; s < 3; ++s) fe[s] = g.lam_E * q[s];
-    return;
-  }
-  const int64_t plane = g.nx * g.ny;
-  const double* px = i > 0 ? Zj + 3 * (c - 1) : (g.dim == 1 ? bj : Zj + 3 * (c + g.nx - 1));
-  const double* py = jy > 0 ? Zj + 3 * (c - g.nx) : Zj + 3 * (c + (g.ny - 1) * g.nx);
-  const double* pz = k > 0 ? Zj + 3 * (c - plane) : bj + 3 * (jy * g.nx + i);
-#pragma unroll
-  for (int s = 0; s < 3; ++s) {
-    double f = __fma_rn(-g.ks, q[s], g.kx * __ldg(px + s));
-    if (g.has_y) f = __fma_rn(g.ky, __ldg(py + s), f);
-    if (g.has_z) f = __fma_rn(g.kz, __ldg(pz + s), f);
-    fe[s] = f;
-  }
-}
 
 template <int KIND>
 __device__ __forceinline__ void implicit_rhs(const FusedParams& p, const double (&q)[3], double (&fi)[3]) {
@@ -215,65 +190,79 @@ __device__ __noinline__ bool newton_exact(const FusedParams& p, const double (&d
   return !singular;
 }
 
-// NS = states available (Z_0..Z_{NS-1}); stage NS, or the final combination
-template <int NS, bool FINAL, int KIND>
-__global__ void __launch_bounds__(kThreads, 2) k_ark_stage(FusedParams p, Geom g, Args a) {
-  __shared__ double red[kThreads / 32][kCols];
-  __shared__ int last;
-  const int t = threadIdx.x;
-  double nu[kMaxNL];
+// One cell of a stage (or of the final combination) from its loaded
+// neighbourhood: ld(j, which, s) returns component s of state j at the cell
+// (which = 0), its x- (1), y- (2) and z-neighbour (3) upwind; the result
+// (Z_i or y_{n+1}) goes to o[3]; ν partials into nu.
+// FULL3D: the tiled kernels' geometry (upwind advection on all three axes)
+// known at compile time, no per-cell operator branches
+template <int NS, bool FINAL, int KIND, bool FULL3D, class Ld>
+__device__ __forceinline__ void ark_cell(const FusedParams& p, const Geom& g, const Args& a, const Ld& ld,
+                                         double (&o)[3], double (&nu)[kMaxNL], int64_t c) {
+  double yn[3], ew[3], acc[3] = {0.0, 0.0, 0.0}, err[3] = {0.0, 0.0, 0.0}, q[3];
 #pragma unroll
-  for (int k = 0; k < kMaxNL; ++k) nu[k] = 0.0;
-  const int64_t plane = g.nx * g.ny;
-  for (int64_t c = (int64_t)blockIdx.x * kThreads + t; c < g.G; c += (int64_t)gridDim.x * kThreads) {
-    const int64_t k = c / plane, rem = c - k * plane, jy = rem / g.nx, i = rem - jy * g.nx;
-    double yn[3], ew[3], acc[3] = {0.0, 0.0, 0.0}, err[3] = {0.0, 0.0, 0.0}, q[3];
+  for (int s = 0; s < 3; ++s) {
+    yn[s] = ld(0, 0, s);
+    const double tt = __fma_rn(p.rtol, fabs(yn[s]), p.atol);
+    ew[s] = safe_mag(tt) ? rcp_nr2(tt) : 1.0 / tt;                     // ewt(y_n) (R30 reciprocal)
+  }
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    double fe[3], fi[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) q[s] = ld(j, 0, s);
+    if (!FULL3D && g.expl == 2) {
+      fe[0] = fe[1] = fe[2] = 0.0;
+    } else if (!FULL3D && g.expl == 1) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) fe[s] = g.lam_E * q[s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {                                    // upwind stencil, contracted
+        double f = __fma_rn(-g.ks, q[s], g.kx * ld(j, 1, s));
+        if (FULL3D || g.has_y) f = __fma_rn(g.ky, ld(j, 2, s), f);
+        if (FULL3D || g.has_z) f = __fma_rn(g.kz, ld(j, 3, s), f);
+        fe[s] = f;
+      }
+    }
+    implicit_rhs<KIND>(p, q, fi);
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      yn[s] = a.y[3 * c + s];
-      ew[s] = 1.0 / __fma_rn(p.rtol, fabs(yn[s]), p.atol);            // ewt(y_n)
-    }
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      const double* Zj = j == 0 ? a.y : a.Z[j - 1];
-#pragma unroll
-      for (int s = 0; s < 3; ++s) q[s] = j == 0 ? yn[s] : Zj[3 * c + s];
-      double fe[3], fi[3];
-      explicit_rhs(g, Zj, a.below[j], c, i, jy, k, q, fe);
-      implicit_rhs<KIND>(p, q, fi);
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        acc[s] = __fma_rn(a.cE[j], fe[s], __fma_rn(a.cI[j], fi[s], acc[s]));
-        if (FINAL) err[s] = __fma_rn(a.cErr[j], fe[s] + fi[s], err[s]);
-      }
-    }
-    if (FINAL) {
-      double w = 0.0;
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        a.out[3 * c + s] = yn[s] + acc[s];
-        const double e = err[s] * ew[s];
-        w = __fma_rn(e, e, w);
-      }
-      nu[0] += w;
-    } else {
-      double d[3], z[3];
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        d[s] = yn[s] + acc[s];
-        z[s] = q[s];                                                   // predictor Z_{i-1}
-      }
-      if (!newton_ct<KIND>(p, d, z, ew, a.krt, nu)) {
-#pragma unroll
-        for (int s = 0; s < 3; ++s) z[s] = q[s];
-        if (!newton_exact<KIND>(p, d, z, ew, a.krt, nu)) atomicMin(a.first, (unsigned long long)(c + 1));
-      }
-#pragma unroll
-      for (int s = 0; s < 3; ++s) a.out[3 * c + s] = z[s];
+      acc[s] = __fma_rn(a.cE[j], fe[s], __fma_rn(a.cI[j], fi[s], acc[s]));
+      if (FINAL) err[s] = __fma_rn(a.cErr[j], fe[s] + fi[s], err[s]);
     }
   }
-  // CTA partials (fixed order), then the last CTA folds every CTA's row
-  const int KC = FINAL ? 1 : a.krt;
+  if (FINAL) {
+    double w = 0.0;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      o[s] = yn[s] + acc[s];
+      const double e = err[s] * ew[s];
+      w = __fma_rn(e, e, w);
+    }
+    nu[0] += w;
+  } else {
+    double d[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      d[s] = yn[s] + acc[s];
+      o[s] = q[s];                                                     // predictor Z_{i-1}
+    }
+    if (!newton_ct<KIND>(p, d, o, ew, a.krt, nu)) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) o[s] = q[s];
+      if (!newton_exact<KIND>(p, d, o, ew, a.krt, nu)) atomicMin(a.first, (unsigned long long)(c + 1));
+    }
+  }
+}
+
+// CTA partials of nu (fixed order), then the last CTA to arrive folds every
+// CTA's row into a.sums (deterministic: lane-strided + shuffle tree)
+template <int NT>
+__device__ __forceinline__ void ark_epilogue(const Args& a, bool fin, double (&nu)[kMaxNL],
+                                             double (&red)[NT / 32][kCols], int& last) {
+  const int t = threadIdx.x;
+  const int KC = fin ? 1 : a.krt;
   const int w = t >> 5, l = t & 31;
 #pragma unroll
   for (int k = 0; k < kMaxNL; ++k) {
@@ -283,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_ark_stage(FusedParams p, Geom g
   __syncthreads();
   if (t >= 1 && t <= KC) {
     double s = red[0][t];
-    for (int q2 = 1; q2 < kThreads / 32; ++q2) s = __dadd_rn(s, red[q2][t]);
+    for (int q2 = 1; q2 < NT / 32; ++q2) s = __dadd_rn(s, red[q2][t]);
     a.partials[(int64_t)blockIdx.x * kCols + t] = s;
     __threadfence();
   }
@@ -292,24 +281,166 @@ __global__ void __launch_bounds__(kThreads, 2) k_ark_stage(FusedParams p, Geom g
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int col = 1 + w; col <= KC; col += kThreads / 32) {
-    double v = 0.0;
-    for (int b = l; b < (int)gridDim.x; b += 32) v = __dadd_rn(v, __ldcg(a.partials + (int64_t)b * kCols + col));
-    v = warp_sum(v);
+  for (int col = 1 + w; col <= KC; col += NT / 32) {
+    // lane-strided with four independent chains (loads in flight), then a
+    // fixed combination and shuffle tree: deterministic
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    const int nb = (int)gridDim.x;
+    int b = l;
+    for (; b + 96 < nb; b += 128) {
+      v0 = __dadd_rn(v0, __ldcg(a.partials + (int64_t)b * kCols + col));
+      v1 = __dadd_rn(v1, __ldcg(a.partials + (int64_t)(b + 32) * kCols + col));
+      v2 = __dadd_rn(v2, __ldcg(a.partials + (int64_t)(b + 64) * kCols + col));
+      v3 = __dadd_rn(v3, __ldcg(a.partials + (int64_t)(b + 96) * kCols + col));
+    }
+    for (; b < nb; b += 32) v0 = __dadd_rn(v0, __ldcg(a.partials + (int64_t)b * kCols + col));
+    double v = warp_sum(__dadd_rn(__dadd_rn(v0, v1), __dadd_rn(v2, v3)));
     if (l == 0) a.sums[col] = v;
   }
   if (t == 0) *a.counter = 0u;
 }
 
-// flags (singular per stage, 0/1) into column 0 of each stage's sums
-__global__ void k_ark_pack(const unsigned long long* first, double* sums) {
+// Plain variant (any geometry): one thread per cell, grid-stride, loads
+// from global memory (neighbours through L1/L2).
+template <int NS, bool FINAL, int KIND>
+__global__ void __launch_bounds__(kThreads, 2) k_ark_stage(FusedParams p, Geom g, Args a) {
+  __shared__ double red[kThreads / 32][kCols];
+  __shared__ int last;
+  double nu[kMaxNL];
+#pragma unroll
+  for (int k = 0; k < kMaxNL; ++k) nu[k] = 0.0;
+  const int64_t plane = g.nx * g.ny;
+  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < g.G; c += (int64_t)gridDim.x * kThreads) {
+    const int64_t k = c / plane, rem = c - k * plane, jy = rem / g.nx, i = rem - jy * g.nx;
+    auto ld = [&](int j, int which, int s) -> double {
+      const double* Zj = j == 0 ? a.y : a.Z[j - 1];
+      const double* b = a.below[j];
+      switch (which) {
+        case 0: return Zj[3 * c + s];
+        case 1: return __ldg((i > 0 ? Zj + 3 * (c - 1) : (g.dim == 1 ? b : Zj + 3 * (c + g.nx - 1))) + s);
+        case 2: return __ldg((jy > 0 ? Zj + 3 * (c - g.nx) : Zj + 3 * (c + (g.ny - 1) * g.nx)) + s);
+        default: return __ldg((k > 0 ? Zj + 3 * (c - plane) : b + 3 * (jy * g.nx + i)) + s);
+      }
+    };
+    double o[3];
+    ark_cell<NS, FINAL, KIND, false>(p, g, a, ld, o, nu, c);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) a.out[3 * c + s] = o[s];
+  }
+  ark_epilogue<kThreads>(a, FINAL, nu, red, last);
+}
+
+// Tiled variant (3D upwind advection, nx % 128 == 0, both transverse axes
+// present): persistent CTAs of 128 threads walk 128-cell tiles; per state
+// the tile, its row-below and plane-below tiles and the two cells before
+// the row start arrive by bulk copies (TMA) into a 2-stage shared ring, the
+// result tile leaves by one bulk store — the fused SBDF step's data path
+// (fused.cu), so the stage runs at the memory system's pace instead of per-
+// thread load latency.
+constexpr int kTile = 128;
+template <int NS, int KS>
+struct __align__(128) ArkTileSmem {
+  double in[KS][NS][3][kTile * 3];
+  double xm[KS][NS][8];
+  double out[2][kTile * 3];
+  uint64_t full[KS];
+  double red[kTile / 32][kCols];
+  int last;
+};
+
+// KS: input stages in the shared ring (2: double-buffered; 1: more CTAs per SM)
+template <int NS, bool FINAL, int KIND, int KS>
+__global__ void __launch_bounds__(kTile) k_ark_tile(FusedParams p, Geom g, Args a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ArkTileSmem<NS, KS>& S = *reinterpret_cast<ArkTileSmem<NS, KS>*>(smem_raw);
+  const int t = threadIdx.x;
+  const int64_t ntiles = g.G / kTile, plane = g.nx * g.ny;
+  constexpr uint32_t kTB = kTile * 3 * 8;
+  auto issue = [&](int64_t tile, int st) {           // thread 0
+    const uint32_t c0 = (uint32_t)(tile * kTile), nx = (uint32_t)g.nx, ny = (uint32_t)g.ny;
+    const uint32_t r = c0 / nx, i0 = c0 - r * nx, jr = r % ny, k = r / ny;
+    const int64_t xprev = i0 > 0 ? (int64_t)c0 - 1 : (int64_t)c0 + g.nx - 1;
+    sunbw::pipe::mbar_expect_tx(&S.full[st], NS * (3 * kTB + 48));
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const double* Zj = j == 0 ? a.y : a.Z[j - 1];
+      sunbw::pipe::bulk_g2s(S.in[st][j][0], Zj + 3 * (int64_t)c0, kTB, &S.full[st]);
+      sunbw::pipe::bulk_g2s(S.in[st][j][1], jr > 0 ? Zj + 3 * ((int64_t)c0 - g.nx) : Zj + 3 * ((int64_t)c0 + (g.ny - 1) * g.nx),
+                     kTB, &S.full[st]);
+      sunbw::pipe::bulk_g2s(S.in[st][j][2], k > 0 ? Zj + 3 * ((int64_t)c0 - plane) : a.below[j] + 3 * ((int64_t)jr * g.nx + i0),
+                     kTB, &S.full[st]);
+      sunbw::pipe::bulk_g2s(S.xm[st][j], Zj + 3 * (xprev - 1), 48, &S.full[st]);
+    }
+  };
+  if (t == 0) {
+    for (int st = 0; st < KS; ++st) sunbw::pipe::mbar_init(&S.full[st], 1);
+    sunbw::pipe::fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int st = 0; st < KS; ++st) {
+      const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+      if (tile < ntiles) issue(tile, st);
+    }
+  double nu[kMaxNL];
+#pragma unroll
+  for (int k = 0; k < kMaxNL; ++k) nu[k] = 0.0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % KS, ob = it & 1;
+    sunbw::pipe::mbar_wait(&S.full[st], (uint32_t)((it / KS) & 1));
+    const double* sb = &S.in[st][0][0][3 * t];        // this cell in the stage's tiles
+    const double* sx = t > 0 ? &S.in[st][0][0][3 * (t - 1)] : &S.xm[st][0][3];
+    const int xs = t > 0 ? 3 * kTile * 3 : 8;          // stride between states of sx
+    auto ld = [&](int j, int which, int s) -> double {
+      switch (which) {
+        case 0: return sb[j * (3 * kTile * 3) + s];
+        case 1: return sx[j * xs + s];
+        case 2: return sb[j * (3 * kTile * 3) + kTile * 3 + s];
+        default: return sb[j * (3 * kTile * 3) + 2 * kTile * 3 + s];
+      }
+    };
+    double o[3];
+    ark_cell<NS, FINAL, KIND, true>(p, g, a, ld, o, nu, tile * kTile + t);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) S.out[ob][3 * t + s] = o[s];
+    sunbw::pipe::fence_async_smem();
+    if (t == 0) sunbw::pipe::bulk_wait_read_all();          // out[ob] of two tiles ago has left
+    __syncthreads();
+    if (t == 0) {
+      sunbw::pipe::bulk_s2g(a.out + tile * (kTile * 3), S.out[ob], kTB);
+      sunbw::pipe::bulk_commit();
+      const int64_t next = tile + KS * (int64_t)gridDim.x;
+      if (next < ntiles) issue(next, st);
+    }
+  }
+  if (t == 0) sunbw::pipe::bulk_wait_all();
+  ark_epilogue<kTile>(a, FINAL, nu, S.red, S.last);
+}
+
+// flags (singular per stage, 0/1) into column 0 of each stage's sums, and
+// the singular records reset for the next round
+__global__ void k_ark_pack(unsigned long long* first, double* sums) {
   const int s = threadIdx.x;
-  if (s < kStages) sums[s * kCols] = first[s] != ~0ull ? 1.0 : 0.0;
+  if (s < kStages) {
+    sums[s * kCols] = first[s] != ~0ull ? 1.0 : 0.0;
+    first[s] = ~0ull;
+  }
 }
 // (global) sums -> [flag, ν_1..ν_4] per stage; the final's column 1 = dsm
 __global__ void k_ark_finalize(const double* sums, double nglobal, double* res) {
   const int t = threadIdx.x;
   if (t < kStages * kCols) res[t] = (t % kCols) == 0 ? sums[t] : __dsqrt_rn(__ddiv_rn(sums[t], nglobal));
+}
+// one rank: both in one launch
+__global__ void k_ark_pack_finalize(unsigned long long* first, double nglobal, double* res, double* sums) {
+  const int t = threadIdx.x;
+  if (t < kStages * kCols) {
+    const int st = t / kCols;
+    res[t] = (t % kCols) == 0 ? (first[st] != ~0ull ? 1.0 : 0.0) : __dsqrt_rn(__ddiv_rn(sums[t], nglobal));
+  }
+  __syncthreads();
+  if (t < kStages) first[t] = ~0ull;
 }
 
 }  // namespace
@@ -333,7 +464,10 @@ struct ArkFused {
   unsigned long long* first = nullptr;
   double* h_res = nullptr;       // pinned
   int kpred[3] = {0, 0, 0};
-  int grid = 1;
+  int grid = 1;                  // plain kernels
+  bool tiled = false;            // 3D upwind, nx % 128 == 0: the TMA-tiled kernels
+  int tgrid[5] = {};             // tiled kernels' persistent grid per NS (1..4)
+  int tgrid_ks[5] = {};          // ... computed for this ring depth
 };
 
 ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal) {
@@ -349,13 +483,17 @@ ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal) {
   for (auto& z : F->Z) ok = ok && cudaMalloc(&z, sizeof(double) * n) == cudaSuccess;
   if (ctx_nranks(ctx) > 1)
     for (auto& hb : F->halo) ok = ok && cudaMalloc(&hb, sizeof(double) * F->geo.halo_len) == cudaSuccess;
-  ok = ok && cudaMalloc(&F->partials, sizeof(double) * F->grid * kCols) == cudaSuccess &&
+  const ArkGeometry& g = F->geo;
+  F->tiled = g.dim == 3 && g.expl == 0 && g.has_y && g.has_z && g.nx % kTile == 0 && g.G % kTile == 0 &&
+             g.G > 0 && g.G < (int64_t(1) << 31);
+  ok = ok && cudaMalloc(&F->partials, sizeof(double) * (int64_t)ctx->nsm * 16 * kCols) == cudaSuccess &&
        cudaMalloc(&F->sums, sizeof(double) * kStages * kCols) == cudaSuccess &&
        cudaMalloc(&F->res, sizeof(double) * kStages * kCols) == cudaSuccess &&
        cudaMalloc(&F->counter, sizeof(unsigned)) == cudaSuccess &&
        cudaMalloc(&F->first, sizeof(unsigned long long) * kStages) == cudaSuccess &&
        cudaHostAlloc(&F->h_res, sizeof(double) * kStages * kCols, cudaHostAllocDefault) == cudaSuccess &&
-       cudaMemsetAsync(F->counter, 0, sizeof(unsigned), ctx->stream) == cudaSuccess;
+       cudaMemsetAsync(F->counter, 0, sizeof(unsigned), ctx->stream) == cudaSuccess &&
+       cudaMemsetAsync(F->first, 0xFF, sizeof(unsigned long long) * kStages, ctx->stream) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     ark_fused_destroy(F);
@@ -381,9 +519,49 @@ void ark_fused_destroy(ArkFused* F) {
 
 namespace {
 
+template <int NS, bool FINAL, int KIND, int KS>
+int launch_tiled_ks(ArkFused* F, const FusedParams& p, const Geom& g, const Args& a) {
+  const int bytes = (int)sizeof(ArkTileSmem<NS, KS>);
+  auto fn = k_ark_tile<NS, FINAL, KIND, KS>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return SUNBW_ERR_CUDA;
+  if (F->tgrid_ks[NS] != KS) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTile, bytes) != cudaSuccess || occ < 1)
+      return SUNBW_ERR_CUDA;
+    const int64_t ntiles = g.G / kTile, cap = (int64_t)F->ctx->nsm * (occ < 16 ? occ : 16);
+    F->tgrid[NS] = (int)(ntiles < cap ? ntiles : cap);
+    F->tgrid_ks[NS] = KS;
+  }
+  fn<<<F->tgrid[NS], kTile, bytes, F->ctx->stream>>>(p, g, a);
+  return 0;
+}
+
+// stages per ring: SUNBW_ARK_KS (1 or 2) overrides, for A/B measurements
+int ark_ks(int NS) {
+  static const int ov = [] {
+    const char* e = std::getenv("SUNBW_ARK_KS");
+    return e ? std::atoi(e) : 0;
+  }();
+  (void)NS;
+  return ov == 1 || ov == 2 ? ov : 1;   // measured: single-buffered rings (more CTAs per SM) are faster
+}
+
+template <int NS, bool FINAL, int KIND>
+int launch_tiled(ArkFused* F, const FusedParams& p, const Geom& g, const Args& a) {
+  return ark_ks(NS) == 1 ? launch_tiled_ks<NS, FINAL, KIND, 1>(F, p, g, a)
+                         : launch_tiled_ks<NS, FINAL, KIND, 2>(F, p, g, a);
+}
+
 template <int KIND>
-int launch_stage(const ArkFused* F, int NS, bool fin, const FusedParams& p, const Geom& g, const Args& a) {
+int launch_stage(ArkFused* F, int NS, bool fin, const FusedParams& p, const Geom& g, const Args& a) {
   cudaStream_t s = F->ctx->stream;
+  if (F->tiled) {
+    if (fin) return launch_tiled<4, true, KIND>(F, p, g, a);
+    if (NS == 1) return launch_tiled<1, false, KIND>(F, p, g, a);
+    if (NS == 2) return launch_tiled<2, false, KIND>(F, p, g, a);
+    return launch_tiled<3, false, KIND>(F, p, g, a);
+  }
   if (fin) {
     k_ark_stage<4, true, KIND><<<F->grid, kThreads, 0, s>>>(p, g, a);
   } else if (NS == 1) {
@@ -430,11 +608,8 @@ int ark_fused_attempt(ArkFused* F, const double* y, double* ynew, double h, doub
   int start = 1;
   int64_t iters = 0;                             // iterations of the stages already accepted (< start)
   for (int round = 0; round < 8; ++round) {
-    if (cudaMemsetAsync(F->first + (start - 1), 0xFF, sizeof(unsigned long long) * (kStages - start + 1),
-                        ctx->stream) != cudaSuccess ||
-        cudaMemsetAsync(F->sums + (start - 1) * kCols, 0, sizeof(double) * (kStages - start + 1) * kCols,
-                        ctx->stream) != cudaSuccess)
-      return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    // (the singular records were reset by the previous round's pack; the
+    // stage sums are overwritten by each launch's fold)
     for (int i = start; i <= 4; ++i) {           // stages start..3, then the final combination (i = 4)
       const bool fin = i == 4;
       Args a{};
@@ -453,21 +628,24 @@ int ark_fused_attempt(ArkFused* F, const double* y, double* ynew, double h, doub
       a.first = F->first + (i - 1);
       a.krt = fin ? 1 : Kr[i];
       if (G0.G > 0) {
-        if (bw_params(F->prob).kind == 1)
-          launch_stage<1>(F, i, fin, p, g, a);
-        else
-          launch_stage<0>(F, i, fin, p, g, a);
+        const int e = bw_params(F->prob).kind == 1 ? launch_stage<1>(F, i, fin, p, g, a)
+                                                   : launch_stage<0>(F, i, fin, p, g, a);
+        if (e) return ctx_set_err(ctx, e);
         ctx->launches++;
         if (ctx_check_launch(ctx)) return SUNBW_ERR_CUDA;
       }
       if (!fin)
         if (int e = exchange(i)) return ctx_set_err(ctx, e);
     }
-    k_ark_pack<<<1, 32, 0, ctx->stream>>>(F->first, F->sums);
-    if (multi)
+    if (multi) {
+      k_ark_pack<<<1, 32, 0, ctx->stream>>>(F->first, F->sums);
       if (int e = ctx->comm->allreduce(F->sums, kStages * kCols, RED_SUM, ctx->stream)) return ctx_set_err(ctx, e);
-    k_ark_finalize<<<1, 32, 0, ctx->stream>>>(F->sums, (double)F->nglobal, F->res);
-    ctx->launches += 2;
+      k_ark_finalize<<<1, 32, 0, ctx->stream>>>(F->sums, (double)F->nglobal, F->res);
+      ctx->launches += 2;
+    } else {
+      k_ark_pack_finalize<<<1, 32, 0, ctx->stream>>>(F->first, (double)F->nglobal, F->res, F->sums);
+      ctx->launches++;
+    }
     if (cudaMemcpyAsync(F->h_res, F->res, sizeof(double) * kStages * kCols, cudaMemcpyDeviceToHost,
                         ctx->stream) != cudaSuccess ||
         cudaStreamSynchronize(ctx->stream) != cudaSuccess)

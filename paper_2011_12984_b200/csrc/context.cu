@@ -10,6 +10,8 @@
 #include <nccl.h>
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -18,6 +20,14 @@
 // ------------------------------------------------------------------ errors
 int ctx_set_err(SUNBW_Context ctx, int code) {
   if (ctx && code < 0 && ctx->err == 0) ctx->err = code;
+  static const bool debug = [] {
+    const char* e = std::getenv("SUNBW_DEBUG");
+    return e && e[0] == '1';
+  }();
+  if (debug && code < 0) {                         // diagnostics: the pending CUDA error, if any
+    const cudaError_t ce = cudaPeekAtLastError();
+    std::fprintf(stderr, "[sunbw] error %d (cuda: %s)\n", code, cudaGetErrorString(ce));
+  }
   return code;
 }
 
@@ -109,6 +119,8 @@ extern "C" int64_t SUNBW_ContextKernelLaunches(SUNBW_Context ctx) {
 extern "C" int SUNBW_ContextRank(SUNBW_Context ctx) { return ctx ? ctx_rank(ctx) : -1; }
 extern "C" int SUNBW_ContextNRanks(SUNBW_Context ctx) { return ctx ? ctx_nranks(ctx) : -1; }
 
+Comm::~Comm() { sunbw::peer_halo_free(peer); }
+
 // -------------------------------------------------------------------- NCCL
 // Reductions finish with ncclAllReduce over NVLink (MPIPlusX global step,
 // P:133-135 §4); the advection halo is a ring shift with ncclSend/Recv (the
@@ -138,6 +150,75 @@ struct NcclComm : Comm {
     return (a == ncclSuccess && b == ncclSuccess && c == ncclSuccess) ? 0 : SUNBW_ERR_COMM;
   }
   bool capturable() const override { return true; }
+  // one process per GPU: IPC handles of every rank's halo buffers, all-
+  // gathered over NCCL, the neighbours' opened here; all ranks agree on the
+  // outcome (allreduce of the local result) before anyone uses it
+  int peer_setup(size_t count, cudaStream_t s) override {
+    if (nranks == 1) return 1;
+    if (peer && sunbw::peer_halo_capacity(peer) >= count) return 0;
+    sunbw::peer_halo_free(peer);
+    peer = nullptr;
+    int ok = sunbw::peer_halo_supported() ? 1 : 0, err = 0;
+    PeerHalo* h = ok ? sunbw::peer_halo_alloc(count, &err) : nullptr;
+    ok = h != nullptr;
+    cudaIpcMemHandle_t mine{};
+    if (ok) ok = cudaIpcGetMemHandle(&mine, sunbw::peer_halo_base(h)) == cudaSuccess;
+    std::vector<char> all(sizeof(cudaIpcMemHandle_t) * nranks);
+    char *d_all = nullptr, *d_mine = nullptr;
+    double* d_ok = nullptr;
+    if (cudaMalloc(&d_all, all.size()) != cudaSuccess || cudaMalloc(&d_mine, sizeof(mine)) != cudaSuccess ||
+        cudaMalloc(&d_ok, sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return 1;
+    }
+    const double okd = ok ? 1.0 : 0.0;
+    cudaMemcpyAsync(d_mine, &mine, sizeof(mine), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_ok, &okd, sizeof(double), cudaMemcpyHostToDevice, s);
+    bool nccl_ok = ncclAllGather(d_mine, d_all, sizeof(mine), ncclChar, comm, s) == ncclSuccess &&
+                   ncclAllReduce(d_ok, d_ok, 1, ncclDouble, ncclMin, comm, s) == ncclSuccess;
+    double all_ok = 0.0;
+    cudaMemcpyAsync(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&all_ok, d_ok, sizeof(double), cudaMemcpyDeviceToHost, s);
+    nccl_ok = nccl_ok && cudaStreamSynchronize(s) == cudaSuccess;
+    cudaFree(d_all);
+    cudaFree(d_mine);
+    cudaFree(d_ok);
+    void *rmap = nullptr, *lmap = nullptr;
+    const int right = (rank + 1) % nranks, left = (rank + nranks - 1) % nranks;
+    int open_ok = 1;
+    if (nccl_ok && all_ok == 1.0) {
+      cudaIpcMemHandle_t hr, hl;
+      std::memcpy(&hr, all.data() + right * sizeof(hr), sizeof(hr));
+      std::memcpy(&hl, all.data() + left * sizeof(hl), sizeof(hl));
+      open_ok = cudaIpcOpenMemHandle(&rmap, hr, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (open_ok) lmap = rmap;
+      if (open_ok && left != right)
+        open_ok = cudaIpcOpenMemHandle(&lmap, hl, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (!open_ok) cudaGetLastError();
+    }
+    // second agreement: every rank opened its neighbours
+    double o2 = (nccl_ok && all_ok == 1.0 && open_ok) ? 1.0 : 0.0, all2 = 0.0;
+    double* d2 = nullptr;
+    if (cudaMalloc(&d2, sizeof(double)) == cudaSuccess) {
+      cudaMemcpyAsync(d2, &o2, sizeof(double), cudaMemcpyHostToDevice, s);
+      if (ncclAllReduce(d2, d2, 1, ncclDouble, ncclMin, comm, s) == ncclSuccess) {
+        cudaMemcpyAsync(&all2, d2, sizeof(double), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) all2 = 0.0;
+      }
+      cudaFree(d2);
+    }
+    if (all2 != 1.0) {
+      if (rmap) cudaIpcCloseMemHandle(rmap);
+      if (lmap && lmap != rmap) cudaIpcCloseMemHandle(lmap);
+      sunbw::peer_halo_free(h);
+      cudaGetLastError();
+      return 1;
+    }
+    sunbw::peer_halo_connect(h, (double*)rmap, (double*)lmap);
+    sunbw::peer_halo_set_ipc(h, rmap, lmap);
+    peer = h;
+    return 0;
+  }
 };
 
 }  // namespace
@@ -200,6 +281,8 @@ __global__ void k_fold_ranks(const double* const* bufs, int nranks, int count,
 
 struct FakeShared {
   int nranks;
+  std::vector<double*> peer_base;       // per rank: its PeerHalo buffer (in-process)
+  std::vector<int> peer_ok;
   std::mutex mu;
   std::condition_variable cv;
   int arrived = 0;
@@ -207,7 +290,7 @@ struct FakeShared {
   std::vector<const double*> ptr;
   std::vector<cudaEvent_t> ev;
   const double** d_ptrs = nullptr;      // device copy of ptr[] per rank slot
-  explicit FakeShared(int n) : nranks(n), ptr(n), ev(n, nullptr) {}
+  explicit FakeShared(int n) : nranks(n), peer_base(n, nullptr), peer_ok(n, 0), ptr(n), ev(n, nullptr) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     int64_t gen = generation;
@@ -277,6 +360,32 @@ struct FakeMember : Comm {
     return cudaGetLastError() == cudaSuccess ? 0 : SUNBW_ERR_CUDA;
   }
   bool capturable() const override { return false; }
+  // in-process ranks on one device: the neighbours' buffers are plain
+  // device pointers of this context
+  int peer_setup(size_t count, cudaStream_t s) override {
+    (void)s;
+    if (nranks == 1) return 1;
+    if (peer && sunbw::peer_halo_capacity(peer) >= count) return 0;
+    sunbw::peer_halo_free(peer);
+    peer = nullptr;
+    int err = 0;
+    PeerHalo* h = sunbw::peer_halo_supported() ? sunbw::peer_halo_alloc(count, &err) : nullptr;
+    sh->peer_base[rank] = h ? sunbw::peer_halo_base(h) : nullptr;
+    sh->peer_ok[rank] = h != nullptr;
+    sh->barrier();
+    bool all = true;
+    for (int q = 0; q < nranks; ++q) all = all && sh->peer_ok[q];
+    const int right = (rank + 1) % nranks, left = (rank + nranks - 1) % nranks;
+    double *rb = sh->peer_base[right], *lb = sh->peer_base[left];
+    sh->barrier();                                   // everyone read the table
+    if (!all) {
+      sunbw::peer_halo_free(h);
+      return 1;
+    }
+    sunbw::peer_halo_connect(h, rb, lb);
+    peer = h;
+    return 0;
+  }
 };
 
 }  // namespace

@@ -151,7 +151,7 @@ const char* nvtx_category(int kind) {
     case BW_K_HALO: case BW_K_ADVECTION: return "advection (incl. halo)";
     case BW_K_REACTION: return "reaction";
     case BW_K_JACOBIAN: case BW_K_SCALEADDI: case BW_K_LU_SETUP: case BW_K_LU_SOLVE: return "linear solve";
-    case BW_K_FUSED_NEWTON: return "fused step (all categories)";
+    case BW_K_FUSED_NEWTON: case BW_K_FUSED_PLANE0: return "fused step (all categories)";
     default: return "other";
   }
 }
@@ -160,7 +160,9 @@ struct Timed {
   Stepper* S;
   int kind;
   bool on;
-  Timed(Stepper* s, int k) : S(s), kind(k), on(s->opt.timing != 0) {
+  cudaStream_t st;
+  Timed(Stepper* s, int k, cudaStream_t stream = nullptr)
+      : S(s), kind(k), on(s->opt.timing != 0), st(stream ? stream : s->ctx->stream) {
     nvtxRangePushA(nvtx_category(k));
     if (!on) return;
     if (S->ev_used + 2 > S->ev_pool.size()) {
@@ -170,13 +172,13 @@ struct Timed {
         S->ev_pool.push_back(e);
       }
     }
-    cudaEventRecordWithFlags(S->ev_pool[S->ev_used], S->ctx->stream,
+    cudaEventRecordWithFlags(S->ev_pool[S->ev_used], st,
                              S->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
   ~Timed() {
     nvtxRangePop();
     if (!on) return;
-    cudaEventRecordWithFlags(S->ev_pool[S->ev_used + 1], S->ctx->stream,
+    cudaEventRecordWithFlags(S->ev_pool[S->ev_used + 1], st,
                              S->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     S->ev_kind.push_back(kind);
     S->ev_used += 2;
@@ -247,18 +249,52 @@ int enqueue_step(Stepper* S, bool first) {
     const bool fold_in_kernel = S->deferred || ctx_nranks(ctx) <= 1;
     // one launch sequence of the step with Kr Newton iterations (tolk: the
     // tolerance-mode kernel, every iteration's nu); with_halo: the P > 1
-    // split around the side-stream halo (a recomputation reuses the halo)
+    // split around the side-stream halo
     auto run = [&](int Kr, bool tolk, bool with_halo) -> int {
       int nb = 0, nb2 = 0;
       sunbw::FusedFold fold{0, S->d_counter, S->deferred ? S->d_pending : nullptr, S->d_scal, S->d_scal + 1,
                             S->d_err, S->nglobal};
       const sunbw::FusedFold* fk = fold_in_kernel ? &fold : nullptr;
-      if (split && with_halo) {
+      if (split && with_halo && ctx->comm->peer) {
+        // copy-engine halo (peer_halo.cu): no SM is needed for the transfer,
+        // so it proceeds while the interior launch fills the GPU
+        const int64_t tpp = fa.nx * fa.ny / 128;          // tiles per z-plane
+        const size_t hl = (size_t)(3 * fa.nx * fa.ny);
+        if (cudaEventRecord(S->evA, ctx->stream) != cudaSuccess ||
+            cudaStreamWaitEvent(S->side, S->evA, 0) != cudaSuccess)
+          return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+        {
+          Timed t(S, BW_K_HALO, S->side);
+          TRY(sunbw::peer_halo_send(ctx->comm->peer, y + 3 * G - hl, hl, S->side) ? ctx_set_err(ctx, SUNBW_ERR_CUDA)
+                                                                                   : 0);
+        }
+        if (cudaEventRecord(S->evB, S->side) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+        {
+          Timed t(S, BW_K_FUSED_NEWTON);
+          TRY(sunbw::fused_newton(ctx, S->prob, G, first, Kr, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
+                                  S->d_partials, S->d_first, &nb, &fa, tpp, -1, nullptr, solver, tolk));
+        }
+        sunbw::FusedAdvection fa0 = fa;
+        if (sunbw::peer_halo_wait(ctx->comm->peer, ctx->stream, &fa0.below)) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+        fold.prev_parts = nb;
+        {
+          Timed t(S, BW_K_FUSED_PLANE0);
+          TRY(sunbw::fused_newton(ctx, S->prob, G, first, Kr, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
+                                  S->d_partials + (int64_t)nb * (Kr + 1), S->d_first, &nb2, &fa0, 0, tpp,
+                                  fk, solver, tolk));
+        }
+        if (sunbw::peer_halo_release(ctx->comm->peer, ctx->stream) ||
+            cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess)   // own send done before y is reused
+          return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      } else if (split && with_halo) {
         const int64_t tpp = fa.nx * fa.ny / 128;          // tiles per z-plane
         if (cudaEventRecord(S->evA, ctx->stream) != cudaSuccess ||
             cudaStreamWaitEvent(S->side, S->evA, 0) != cudaSuccess)
           return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-        TRY(sunbw::bw_halo_stream(S->prob, y, S->side));
+        {
+          Timed t(S, BW_K_HALO, S->side);
+          TRY(sunbw::bw_halo_stream(S->prob, y, S->side));
+        }
         if (cudaEventRecord(S->evB, S->side) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
         {
           Timed t(S, BW_K_FUSED_NEWTON);
@@ -268,7 +304,7 @@ int enqueue_step(Stepper* S, bool first) {
         if (cudaStreamWaitEvent(ctx->stream, S->evB, 0) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
         fold.prev_parts = nb;
         {
-          Timed t(S, BW_K_FUSED_NEWTON);
+          Timed t(S, BW_K_FUSED_PLANE0);
           TRY(sunbw::fused_newton(ctx, S->prob, G, first, Kr, h, o.rtol, o.atol, y, nullptr, fEp, fE, z,
                                   S->d_partials + (int64_t)nb * (Kr + 1), S->d_first, &nb2, &fa, 0, tpp,
                                   fk, solver, tolk));
@@ -297,7 +333,9 @@ int enqueue_step(Stepper* S, bool first) {
     // recoverable failure, as on the composed path.
     int Kr = S->k_pred > 0 && S->k_pred <= o.K ? S->k_pred : o.K;
     for (int attempt = 0; attempt < 3; ++attempt) {
-      TRY(run(Kr, true, attempt == 0));
+      // every attempt repeats the halo exchange: the copy-engine halo's slot
+      // is released to the sender after each plane-0 launch
+      TRY(run(Kr, true, true));
       TRY(sunbw::or_flags_over_ranks(ctx, S->d_first, S->d_err));
       if (cudaMemcpyAsync(S->h_tol, S->d_scal, sizeof(double) * (Kr + 1), cudaMemcpyDeviceToHost,
                           ctx->stream) != cudaSuccess ||
@@ -566,6 +604,11 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
         cudaEventCreateWithFlags(&S->evB, cudaEventDisableTiming) != cudaSuccess)
       e = SUNBW_ERR_CUDA;
     if (!e) e = alloc(S, &S->d_pending, kMaxK + 2);
+    // copy-engine halo for the fused step (collective; falls back to NCCL
+    // send/recv when peer mappings are unavailable on any rank)
+    sunbw::FusedAdvection fa;
+    if (!e && opt->fused_advection && sunbw::bw_fused_advection(prob, y0->d, &fa))
+      ctx->comm->peer_setup((size_t)(3 * fa.nx * fa.ny), ctx->stream);
   }
   if (!e) e = alloc(S, &S->d_scal, kMaxK + 8);
   if (!e) e = alloc(S, &S->d_partials, (int64_t)(ctx->nsm * 16) * (kMaxK + 1));

@@ -17,9 +17,15 @@
 // ------------------------------------------------------------ communicator
 enum RedOp { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
 
+struct PeerHalo;   // peer_halo.cu
+
 struct Comm {
   int rank = 0, nranks = 1;
-  virtual ~Comm() {}
+  PeerHalo* peer = nullptr;            // copy-engine halo into the right neighbour (peer_halo.cu)
+  virtual ~Comm();
+  // collective: make `peer` ready for halos of up to `count` doubles;
+  // 0 = ready, > 0 = not available (the caller uses halo_shift)
+  virtual int peer_setup(size_t count, cudaStream_t s) { (void)count; (void)s; return 1; }
   // in-place allreduce of `count` doubles in device memory, on stream s
   virtual int allreduce(double* d_buf, int count, RedOp op, cudaStream_t s) = 0;
   // ring shift: send `count` doubles to rank+1, receive from rank-1
@@ -27,6 +33,23 @@ struct Comm {
                          cudaStream_t s) = 0;
   virtual bool capturable() const = 0;   // may run inside CUDA graph capture
 };
+
+namespace sunbw {
+bool peer_halo_supported();
+PeerHalo* peer_halo_alloc(size_t cap, int* err);
+void peer_halo_free(PeerHalo* h);
+double* peer_halo_base(PeerHalo* h);
+size_t peer_halo_capacity(const PeerHalo* h);
+void peer_halo_connect(PeerHalo* h, double* right_base, double* left_base);
+void peer_halo_set_ipc(PeerHalo* h, void* right_map, void* left_map);
+// sender (side stream): wait until the right neighbour freed the slot, copy
+// `send` into it, raise its arrival flag
+int peer_halo_send(PeerHalo* h, const double* send, size_t count, cudaStream_t side);
+// receiver (main stream): wait for this exchange's data; *recv = the slot
+int peer_halo_wait(PeerHalo* h, cudaStream_t main, const double** recv);
+// receiver (main stream, after the consumer kernel): free the slot
+int peer_halo_release(PeerHalo* h, cudaStream_t main);
+}  // namespace sunbw
 
 Comm* make_nccl_comm(const void* uid, int rank, int nranks, int* err);
 Comm* make_fake_comm_member(void* shared, int rank, int* err);

@@ -29,9 +29,10 @@ SUNBW_POLICY_THREAD_DIRECT = 1
 SUNBW_RECOV_SINGULAR, SUNBW_RECOV_NONCONV, SUNBW_RECOV_BAD_EWT = 1, 2, 3
 (BW_K_HALO, BW_K_ADVECTION, BW_K_RHS_COMBINE, BW_K_EWT, BW_K_PREDICT, BW_K_JACOBIAN,
  BW_K_SCALEADDI, BW_K_LU_SETUP, BW_K_REACTION, BW_K_RESIDUAL, BW_K_LU_SOLVE, BW_K_UPDATE,
- BW_K_WRMS, BW_K_FUSED_NEWTON, BW_K_COUNT_) = range(15)
+ BW_K_WRMS, BW_K_FUSED_NEWTON, BW_K_FUSED_PLANE0, BW_K_COUNT_) = range(16)
 KERNEL_NAMES = ["halo", "advection", "rhs_combine", "ewt", "predict", "jacobian", "scaleaddi",
-                "lu_setup", "reaction", "residual", "lu_solve", "update", "wrms", "fused_newton"]
+                "lu_setup", "reaction", "residual", "lu_solve", "update", "wrms", "fused_newton",
+                "fused_plane0"]
 
 
 class BW_BrussParams(C.Structure):

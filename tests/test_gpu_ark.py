@@ -83,26 +83,29 @@ def test_ark_3D_and_retries(S, ctx, fused):
     assert rc == 1 and st["rejected_nl"] == 5 and st["accepted"] == 0
 
 
-def test_ark_fused_C3_shape(S, ctx):
-    """The bench's ARK row: C3-shaped grid (reduced to 64^3 here for the
-    oracle's time) to t = 0.003, fused stages vs the oracle."""
-    n = 64
-    y0 = oracle.bruss_ic(n, n, n)
-    k = 0.01 * n
-    rc2, yref, st2 = oracle.ark_integrate(y0, 0.003, h0=1e-4, nx=n, ny=n, nz=n, kx=k, ky=k, kz=k)
-    rc, y, st = run(S, ctx, S.bruss_params(dim=3, nx=n, ny=n, nz=n), y0, 0.003, h0=1e-4, fused=True)
+@pytest.mark.parametrize("shape", [(64, 64, 64), (128, 24, 16)])
+def test_ark_fused_C3_shape(S, ctx, shape):
+    """The bench's ARK row: C3-shaped grids (reduced for the oracle's time)
+    to t = 0.003, fused stages vs the oracle; nx = 128 takes the TMA-tiled
+    stage kernels, nx = 64 the plain ones."""
+    nx, ny, nz = shape
+    y0 = oracle.bruss_ic(nx, ny, nz)
+    rc2, yref, st2 = oracle.ark_integrate(y0, 0.003, h0=1e-4, nx=nx, ny=ny, nz=nz, kx=0.01 * nx, ky=0.01 * ny,
+                                          kz=0.01 * nz)
+    rc, y, st = run(S, ctx, S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz), y0, 0.003, h0=1e-4, fused=True)
     assert rc == rc2 == 0
     for key in ("accepted", "rejected_err", "rejected_nl", "newton_iters", "setups"):
         assert st[key] == st2[key], key
     assert rel(y, yref) <= 1e-9
 
 
-def test_ark_fused_multirank(S):
+@pytest.mark.parametrize("shape", [(12, 10, 8), (128, 6, 8)])
+def test_ark_fused_multirank(S, shape):
     """P = 2 logical ranks (fake communicator): the stage halos and the
     per-attempt allreduce of all stage norms; same counts and state as the
-    one-rank oracle run."""
+    one-rank oracle run (plain and TMA-tiled stage kernels)."""
     from test_gpu_bruss import run_ranks
-    nx, ny, nz = 12, 10, 8
+    nx, ny, nz = shape
     y0 = oracle.bruss_ic(nx, ny, nz)
     params = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz)
     rc2, yref, st2 = oracle.ark_integrate(y0, 0.02, h0=1e-4, nx=nx, ny=ny, nz=nz, kx=0.01 * nx,

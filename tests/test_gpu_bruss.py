@@ -537,3 +537,42 @@ def test_fused_multistep_small_problems(S, ctx, case):
         assert abs(stats["last_nu"] - stref["last_nu"]) <= 1e-12 * stref["last_nu"]
         outs.append(launches)
     assert outs[0] < outs[1]                           # far fewer launches in one-launch mode
+
+
+@pytest.mark.parametrize("peer", ["1", "0"])
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_multirank_fused_copy_engine_halo(S, nranks, peer, monkeypatch):
+    """The fused step at P > 1 with the halo plane moved by the copy engine
+    into the right neighbour's double-buffered slot (peer_halo.cu: stream
+    memory-op flags, no SM, overlapping the interior launch) or, with
+    SUNBW_PEER_HALO=0, by the communicator's send/recv: bit-identical to the
+    oracle either way, and the split step's timing kinds (halo on the side
+    stream, interior, plane 0) are reported."""
+    monkeypatch.setenv("SUNBW_PEER_HALO", peer)
+    nx, ny, nzl, steps = 128, 8, 4, 6
+    nz = nzl * nranks
+    y0 = oracle.bruss_ic(nx, ny, nz)
+    params = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz)
+    k = kappas(nx, ny, nz)
+    _, yref, _, _ = oracle.sbdf_integrate(y0, steps, kind=0, K=3, nx=nx, ny=ny, nz=nz, kx=k[0], ky=k[1], kz=k[2],
+                                          h=1e-3)
+
+    def fn(c, r):
+        P = S.Problem(c, params)
+        n, off = 3 * P.local_cells, 3 * P.cell_offset
+        y = torch.from_numpy(y0[off:off + n].copy()).cuda()
+        yout = torch.empty_like(y)
+        st = S.Stepper(P, S.NVector(c, y), S.stepper_options(h=1e-3, K=3, use_graph=False, fused=True,
+                                                              timing=True))
+        rc, _ = st.advance(steps, S.NVector(c, yout))
+        c.stream.synchronize()
+        kt = st.kernel_times()
+        res = (rc, off, yout.cpu().numpy(), set(kt))
+        st.destroy(); P.destroy()
+        return res
+
+    res = run_ranks(S, nranks, fn)
+    assert all(r[0] == 0 for r in res)
+    assert all({"halo", "fused_newton", "fused_plane0"} <= r[3] for r in res), res[0][3]
+    y = np.concatenate([r[2] for r in sorted(res, key=lambda t: t[1])])
+    assert_bits_equal(y, yref, f"P={nranks} peer={peer}")
