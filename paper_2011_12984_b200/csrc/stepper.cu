@@ -99,6 +99,7 @@ struct Stepper {
   int* d_err;            // 1: non-positive ewt denominator seen
   double* d_partials;    // fused mode per-CTA partials
   double* h_tol = nullptr;   // fused tolerance mode: pinned [min, nu_1..nu_8 | first | err]
+  unsigned long long* h_end = nullptr;   // pinned: end-of-Advance [first, err, nu]
   int k_pred = 0;            // fused tolerance mode: the last step's iteration count
   int64_t tol_launches = 0;  // fused tolerance mode: step launches (recomputations included)
   unsigned* d_counter = nullptr;   // fused mode: arrival counter of the in-kernel fold
@@ -117,13 +118,15 @@ struct Stepper {
   BW_StepperStats st{};
   // graphs, keyed by rotation state (iy, ife): 3 × 2
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t gexec[6] = {};
-  int64_t graph_launches[6] = {};
+  // keys 0..5: one step; 6..11: a chain of kChain steps starting at that
+  // rotation state (the rotation's period), replayed while >= kChain remain
+  cudaGraphExec_t gexec[12] = {};
+  int64_t graph_launches[12] = {};
   // timing mode with graphs: the captured graph's event-record nodes (in
   // capture order, start/end pairs) get fresh pool events before each replay
-  cudaGraph_t graph[6] = {};
-  std::vector<cudaGraphNode_t> ev_nodes[6];
-  std::vector<int> ev_node_kind[6];
+  cudaGraph_t graph[12] = {};
+  std::vector<cudaGraphNode_t> ev_nodes[12];
+  std::vector<int> ev_node_kind[12];
   bool capturing = false;
   // timing
   std::vector<cudaEvent_t> ev_pool;
@@ -413,10 +416,12 @@ int enqueue_step(Stepper* S, bool first) {
     TRY(sunbw::or_flags_over_ranks(ctx, S->d_first, S->d_err));
     unsigned long long f = 0;
     int err = 0;
-    if (cudaMemcpyAsync(&f, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
-        cudaMemcpyAsync(&err, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+    if (cudaMemcpyAsync(S->h_end, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(S->h_end + 1, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
         cudaStreamSynchronize(ctx->stream) != cudaSuccess)
       return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    std::memcpy(&f, S->h_end, sizeof(f));
+    std::memcpy(&err, S->h_end + 1, sizeof(int));
     if (err) return SUNBW_RECOV_BAD_EWT;
     if (f != ~0ull) { S->st.singular = (int64_t)f; return SUNBW_RECOV_SINGULAR; }
   }
@@ -466,8 +471,11 @@ void rotate(Stepper* S) {
 
 int graph_key(const Stepper* S) { return S->iy * 2 + S->ife; }
 
-// capture one SBDF2 step (fixed-K) for the current rotation state
-int capture_step(Stepper* S, int key) {
+constexpr int kChain = 6;
+
+// capture `nsteps` SBDF2 steps (fixed-K) from the current rotation state into
+// graph `key` (the rotation state is restored afterwards)
+int capture_step(Stepper* S, int key, int nsteps = 1) {
   SUNBW_Context ctx = S->ctx;
   if (!S->cap_stream &&
       cudaStreamCreateWithFlags(&S->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -483,7 +491,12 @@ int capture_step(Stepper* S, int key) {
     rc = SUNBW_ERR_CUDA;
   } else {
     S->capturing = true;
-    rc = enqueue_step(S, false);
+    const int iy = S->iy, iyp = S->iyp, iz = S->iz, ife = S->ife, ifep = S->ifep;
+    for (int k = 0; k < nsteps && !rc; ++k) {
+      rc = enqueue_step(S, false);
+      rotate(S);
+    }
+    S->iy = iy; S->iyp = iyp; S->iz = iz; S->ife = ife; S->ifep = ifep;
     S->capturing = false;
     if (cudaStreamEndCapture(S->cap_stream, &g) != cudaSuccess) rc = rc ? rc : SUNBW_ERR_CUDA;
   }
@@ -539,9 +552,11 @@ int capture_all_keys(Stepper* S) {
   int rc = 0;
   for (int r = 0; r < 6 && !rc; ++r) {
     const int key = graph_key(S);
-    if (!S->gexec[key]) {
-      rc = capture_step(S, key);
-      if (!rc && cudaGraphUpload(S->gexec[key], S->ctx->stream) != cudaSuccess)
+    for (int c = 0; c < 2 && !rc; ++c) {          // the single step, then the chain
+      const int gk = key + 6 * c;
+      if (S->gexec[gk]) continue;
+      rc = capture_step(S, gk, c ? kChain : 1);
+      if (!rc && cudaGraphUpload(S->gexec[gk], S->ctx->stream) != cudaSuccess)
         rc = ctx_set_err(S->ctx, SUNBW_ERR_CUDA);
     }
     rotate(S);
@@ -615,6 +630,8 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   if (!e && cudaMalloc(&S->d_first, sizeof(unsigned long long)) != cudaSuccess) e = SUNBW_ERR_MEM;
   if (!e && cudaMalloc(&S->d_err, sizeof(int)) != cudaSuccess) e = SUNBW_ERR_MEM;
   if (!e && cudaMalloc(&S->d_counter, sizeof(unsigned)) != cudaSuccess) e = SUNBW_ERR_MEM;
+  if (!e && cudaHostAlloc(&S->h_end, 4 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
+    e = SUNBW_ERR_MEM;
   if (!e && opt->fused && opt->newton_mode == 1 &&
       cudaHostAlloc(&S->h_tol, sizeof(double) * (kMaxKF + 4), cudaHostAllocDefault) != cudaSuccess)
     e = SUNBW_ERR_MEM;
@@ -661,13 +678,18 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
     S->st.newton_iters += nsteps * S->opt.K;
   }
   const int64_t nloop = S->small ? 0 : nsteps;  // per-step launches
-  for (int64_t s = 0; s < nloop; ++s) {
+  for (int64_t s = 0; s < nloop;) {
     bool first = S->step == 0;
+    int nin = 1;                                  // steps done by this iteration
     if (S->opt.use_graph && !first) {
       int key = graph_key(S);
       if (!S->gexec[key]) {
         int e = capture_all_keys(S);
         if (e) return e;
+      }
+      if (nloop - s >= kChain && S->gexec[key + 6]) {   // kChain steps in one graph launch
+        key += 6;
+        nin = kChain;
       }
       if (S->opt.timing && !S->ev_nodes[key].empty()) {
         const std::vector<cudaGraphNode_t>& nodes = S->ev_nodes[key];
@@ -687,8 +709,8 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
       }
       if (cudaGraphLaunch(S->gexec[key], ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
       ctx->launches += S->graph_launches[key];
-      S->st.newton_iters += S->opt.K;
-      S->st.solves += S->opt.fused ? 0 : S->opt.K;
+      S->st.newton_iters += (int64_t)nin * S->opt.K;
+      S->st.solves += S->opt.fused ? 0 : (int64_t)nin * S->opt.K;
     } else {
       int64_t it0 = S->st.newton_iters;
       rc = enqueue_step(S, first);
@@ -696,11 +718,14 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
       if (rc < 0) return rc;
       if (rc > 0) { S->st.fails++; break; }
     }
-    S->st.setups++;
-    rotate(S);
-    S->step++;
-    S->t += S->opt.h;
-    S->st.steps++;
+    for (int k = 0; k < nin; ++k) {
+      S->st.setups++;
+      rotate(S);
+      S->step++;
+      S->t += S->opt.h;
+      S->st.steps++;
+    }
+    s += nin;
   }
   // end of the call: one synchronisation for the deferred checks
   unsigned long long f = 0;
@@ -716,15 +741,23 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
     TRY(sunbw::or_flags_over_ranks(ctx, S->d_first, S->d_err));
   }
   if (S->opt.newton_mode == 0) {
-    if (cudaMemcpyAsync(&f, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
-        cudaMemcpyAsync(&err, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
-        cudaMemcpyAsync(&nu, S->d_scal + S->opt.K, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+    // into pinned memory: asynchronous copies, one synchronisation below
+    // (pageable destinations would each block in a staging copy)
+    if (cudaMemcpyAsync(S->h_end, S->d_first, sizeof(f), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(S->h_end + 1, S->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(S->h_end + 2, S->d_scal + S->opt.K, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream) !=
+            cudaSuccess)
       return ctx_set_err(ctx, SUNBW_ERR_CUDA);
   }
   if (y_out &&
       cudaMemcpyAsync(y_out->d, S->y[S->iy], sizeof(double) * S->n, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  if (S->opt.newton_mode == 0) {
+    std::memcpy(&f, S->h_end, sizeof(f));
+    std::memcpy(&err, S->h_end + 1, sizeof(int));
+    std::memcpy(&nu, S->h_end + 2, sizeof(double));
+  }
   // timing events are read lazily (BW_StepperKernelTimes, or the next call
   // once many are pending): no host work after the step kernels here
   if (S->opt.timing && S->ev_used > 4096) harvest_timing(S);
@@ -794,6 +827,7 @@ extern "C" int BW_StepperDestroy(void* stepper) {
   if (S->evB) cudaEventDestroy(S->evB);
   if (S->d_pending) cudaFree(S->d_pending);
   if (S->h_tol) cudaFreeHost(S->h_tol);
+  if (S->h_end) cudaFreeHost(S->h_end);
   delete S;
   return 0;
 }

@@ -5,6 +5,10 @@
 //   mode 0: y_n + H_n in, y_{n+1} + H_{n+1} out          (4 streams, 96 B/cell)
 //   mode 1: mode 0 + the row-below and plane-below tiles  (the fused step's pattern)
 //   mode 2: mode 1 with a dependent fp64 chain of `chain` ops per cell
+//   mode 3: mode 1 in the packed working layout [y | H] per tile: one 6 KB
+//           bulk load + the two neighbour y tiles, one 6 KB bulk store
+//           (3 address streams instead of 5)
+//   mode 4: mode 3 without the neighbour tiles (2 streams)
 // Prints us per launch and algorithmic GB/s (96 B/cell) per mode.
 #include <cstdint>
 #include <cstdio>
@@ -34,8 +38,21 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
   extern __shared__ __align__(128) unsigned char raw[];
   Smem& S = *reinterpret_cast<Smem*>(raw);
   const int t = threadIdx.x;
+  const bool packed = mode >= 3;
   auto issue = [&](int64_t tile, int st) {
-    const bool nb = mode >= 1;
+    const bool nb = mode >= 1 && mode != 4;
+    if (packed) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&S.full[st])),
+                   "r"((nb ? 4 : 2) * kTile * 8) : "memory");
+      g2s(S.in[st][0], y + tile * 2 * kTile, 2 * kTile * 8, &S.full[st]);
+      if (nb) {
+        const int64_t ym = tile >= row_tiles ? tile - row_tiles : tile;
+        const int64_t zm = tile >= plane_tiles ? tile - plane_tiles : tile + ntiles - plane_tiles;
+        g2s(S.in[st][2], y + ym * 2 * kTile, kTile * 8, &S.full[st]);
+        g2s(S.in[st][3], y + zm * 2 * kTile, kTile * 8, &S.full[st]);
+      }
+      return;
+    }
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&S.full[st])),
                  "r"((nb ? 4 : 2) * kTile * 8) : "memory");
     g2s(S.in[st][0], y + tile * kTile, kTile * 8, &S.full[st]);
@@ -64,7 +81,7 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
       double a = S.in[st][0][3 * t + s], b = S.in[st][1][3 * t + s];
-      if (mode >= 1) a = __dadd_rn(a, __dadd_rn(S.in[st][2][3 * t + s], S.in[st][3][3 * t + s]));
+      if (mode >= 1 && mode != 4) a = __dadd_rn(a, __dadd_rn(S.in[st][2][3 * t + s], S.in[st][3][3 * t + s]));
       if (mode == 2)
         for (int c = 0; c < chain; ++c) a = __fma_rn(a, 0.999999, b);
       S.out[ob][0][3 * t + s] = a;
@@ -74,8 +91,12 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
     if (t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncthreads();
     if (t == 0) {
-      s2g(z + tile * kTile, S.out[ob][0], kTile * 8);
-      s2g(ho + tile * kTile, S.out[ob][1], kTile * 8);
+      if (packed) {
+        s2g(z + tile * 2 * kTile, S.out[ob][0], 2 * kTile * 8);
+      } else {
+        s2g(z + tile * kTile, S.out[ob][0], kTile * 8);
+        s2g(ho + tile * kTile, S.out[ob][1], kTile * 8);
+      }
       const int64_t nx = tile + 2 * (int64_t)gridDim.x;
       if (nx < ntiles) issue(nx, st);
     }
@@ -87,14 +108,15 @@ int main() {
   const int64_t n = 256, G = n * n * n, ntiles = G / kCells;
   double *y, *h, *z, *ho;
   const size_t bytes = (size_t)G * 3 * 8;
-  cudaMalloc(&y, bytes); cudaMalloc(&h, bytes); cudaMalloc(&z, bytes); cudaMalloc(&ho, bytes);
-  cudaMemset(y, 0, bytes); cudaMemset(h, 0, bytes);
+  // packed modes use y and z as [y | H] arrays of 2x the size
+  cudaMalloc(&y, 2 * bytes); cudaMalloc(&h, bytes); cudaMalloc(&z, 2 * bytes); cudaMalloc(&ho, bytes);
+  cudaMemset(y, 0, 2 * bytes); cudaMemset(h, 0, bytes);
   const int smem = sizeof(Smem);
   cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const int grid = nsm * 5;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  struct { int mode, chain; } cases[] = {{0, 0}, {1, 0}, {2, 32}, {2, 64}, {2, 128}, {2, 256}};
+  struct { int mode, chain; } cases[] = {{0, 0}, {1, 0}, {3, 0}, {4, 0}, {1, 0}, {3, 0}, {2, 32}, {2, 64}};
   for (auto c : cases) {
     for (int w = 0; w < 3; ++w)
       k_tiles<<<grid, kCells, smem>>>(y, h, z, ho, ntiles, 2, 512, c.mode, c.chain);
