@@ -9,9 +9,13 @@
 //           bulk load + the two neighbour y tiles, one 6 KB bulk store
 //           (3 address streams instead of 5)
 //   mode 4: mode 3 without the neighbour tiles (2 streams)
+//   mode 5: mode 1 with L2 cache hints: the own y tile evict_last (it is read
+//           again as a neighbour), neighbour tiles evict_first (last use),
+//           H and both stores evict_first
 // Prints us per launch and algorithmic GB/s (96 B/cell) per mode.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int kCells = 128, kTile = kCells * 3;
@@ -20,6 +24,27 @@ __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_
 __device__ __forceinline__ void g2s(void* d, const void* s, uint32_t n, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(d)),
                "l"(s), "r"(n), "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void g2s_h(void* d, const void* s, uint32_t n, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          sa(d)),
+      "l"(s), "r"(n), "r"(sa(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void s2g_h(void* d, const void* s, uint32_t n, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(d), "r"(sa(s)),
+               "r"(n), "l"(pol) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void s2g(void* d, const void* s, uint32_t n) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d), "r"(sa(s)), "r"(n) : "memory");
@@ -38,7 +63,9 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
   extern __shared__ __align__(128) unsigned char raw[];
   Smem& S = *reinterpret_cast<Smem*>(raw);
   const int t = threadIdx.x;
-  const bool packed = mode >= 3;
+  const bool packed = mode == 3 || mode == 4;
+  const bool hints = mode == 5;
+  const uint64_t PL = pol_last(), PF = pol_first();
   auto issue = [&](int64_t tile, int st) {
     const bool nb = mode >= 1 && mode != 4;
     if (packed) {
@@ -55,6 +82,15 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
     }
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&S.full[st])),
                  "r"((nb ? 4 : 2) * kTile * 8) : "memory");
+    if (hints) {
+      const int64_t ym = tile >= row_tiles ? tile - row_tiles : tile;
+      const int64_t zm = tile >= plane_tiles ? tile - plane_tiles : tile + ntiles - plane_tiles;
+      g2s_h(S.in[st][0], y + tile * kTile, kTile * 8, &S.full[st], PL);
+      g2s_h(S.in[st][1], h + tile * kTile, kTile * 8, &S.full[st], PF);
+      g2s_h(S.in[st][2], y + ym * kTile, kTile * 8, &S.full[st], PL);
+      g2s_h(S.in[st][3], y + zm * kTile, kTile * 8, &S.full[st], PF);
+      return;
+    }
     g2s(S.in[st][0], y + tile * kTile, kTile * 8, &S.full[st]);
     g2s(S.in[st][1], h + tile * kTile, kTile * 8, &S.full[st]);
     if (nb) {
@@ -93,6 +129,9 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
     if (t == 0) {
       if (packed) {
         s2g(z + tile * 2 * kTile, S.out[ob][0], 2 * kTile * 8);
+      } else if (hints) {
+        s2g_h(z + tile * kTile, S.out[ob][0], kTile * 8, PF);
+        s2g_h(ho + tile * kTile, S.out[ob][1], kTile * 8, PF);
       } else {
         s2g(z + tile * kTile, S.out[ob][0], kTile * 8);
         s2g(ho + tile * kTile, S.out[ob][1], kTile * 8);
@@ -104,7 +143,7 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
   if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int64_t n = 256, G = n * n * n, ntiles = G / kCells;
   double *y, *h, *z, *ho;
   const size_t bytes = (size_t)G * 3 * 8;
@@ -116,8 +155,10 @@ int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const int grid = nsm * 5;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  struct { int mode, chain; } cases[] = {{0, 0}, {1, 0}, {3, 0}, {4, 0}, {1, 0}, {3, 0}, {2, 32}, {2, 64}};
+  int only = argc > 1 ? atoi(argv[1]) : -1;
+  struct { int mode, chain; } cases[] = {{0, 0}, {1, 0}, {3, 0}, {4, 0}, {5, 0}, {1, 0}, {5, 0}, {2, 32}, {2, 64}};
   for (auto c : cases) {
+    if (only >= 0 && c.mode != only) continue;
     for (int w = 0; w < 3; ++w)
       k_tiles<<<grid, kCells, smem>>>(y, h, z, ho, ntiles, 2, 512, c.mode, c.chain);
     cudaEventRecord(e0);
