@@ -1,0 +1,12 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:fused_newton -s 3 -c 1 -o gpurun_out/prof_ct python bench.py --steps 5 --warmup 3 --no-ops --no-cpu > /dev/null 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:fused_newton -s 3 -c 1 -o gpurun_out/prof_ex python bench.py --steps 5 --warmup 3 --no-ops --no-cpu --numerics exact > /dev/null 2>&1
+python tools/traffic_json.py gpurun_out/prof_ct.ncu-rep gpurun_out/prof_ex.ncu-rep > /dev/null 2>&1; cp profiles/ncu_traffic.json gpurun_out/
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 600 gpurun_out/bench_default.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_fused.csv python bench.py --steps 5 --warmup 3 --no-ops --no-cpu > /dev/null 2>&1
+timeout 300 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2>&1; tail -c 300 gpurun_out/bench_ref.json
+python tools/ncu_summary.py gpurun_out/prof_ct.ncu-rep > gpurun_out/ncu_summary_ct.txt 2>&1
+python tools/ncu_summary.py gpurun_out/prof_ex.ncu-rep > gpurun_out/ncu_summary_ex.txt 2>&1
+rm -f gpurun_out/prof_ex.ncu-rep
