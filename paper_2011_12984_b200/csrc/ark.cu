@@ -220,7 +220,12 @@ extern "C" int BW_ArkEvolve(void* ark, double t_end, N_Vector y_out, BW_ArkStats
   if (y_out && (y_out->ctx != ctx || y_out->local_len != A->n)) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
   int rc = 0;
   int attempts = 0;
-  while (t_end - A->t > 1e-12 * std::fmax(1.0, std::fabs(t_end))) {
+  if (A->fused) {                                // the same loop, decided on the device (R33)
+    if (int e = sunbw::ark_fused_evolve(A->fused, &A->y, &A->ynew, &A->t, &A->h, t_end, A->opt, &A->st, &rc))
+      return e;
+    attempts = -1;                               // (loop below skipped)
+  }
+  while (attempts >= 0 && t_end - A->t > 1e-12 * std::fmax(1.0, std::fabs(t_end))) {
     if (attempts++ >= A->opt.max_steps) { rc = 1; break; }
     // a step shortened to land on t_end does not shrink the next proposal
     // (DESIGN R26): the unclipped h is restored after it if larger
@@ -230,10 +235,7 @@ extern "C" int BW_ArkEvolve(void* ark, double t_end, N_Vector y_out, BW_ArkStats
     if (A->h < 1e-14 * (1.0 + A->t)) { rc = 2; break; }
     int nl_ok = 1;
     double dsm = 0.0;
-    int e = A->fused ? sunbw::ark_fused_attempt(A->fused, A->y, A->ynew, A->h, A->opt.rtol, A->opt.atol,
-                                                A->opt.tol_nl, A->opt.maxnl, &nl_ok, &dsm,
-                                                &A->st.newton_iters, &A->st.setups)
-                     : attempt(A, &nl_ok, &dsm);
+    int e = attempt(A, &nl_ok, &dsm);
     if (e < 0) return e;
     if (!nl_ok) {
       A->st.rejected_nl++;

@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "sunbw_internal.h"
 #include "cellstep.cuh"
@@ -47,25 +48,26 @@ constexpr int kMaxNL = 4;                // fused ARK: Newton iterations per sta
 constexpr int kCols = kMaxNL + 1;        // partial columns: [unused, S_1..S_kMaxNL]
 constexpr int kStages = 4;               // ARK3(2)4L[2]SA
 
-// ARK3(2)4L[2]SA (Kennedy & Carpenter 2003), as in ark.cu / the oracle
-const double kG = 1767732205903.0 / 4055673282236.0;
-const double kAE[4][4] = {
+// ARK3(2)4L[2]SA (Kennedy & Carpenter 2003), as in ark.cu / the oracle, for
+// the kernels (constant-folded from the same literals as ark.cu's host copy)
+__constant__ double d_kG = 1767732205903.0 / 4055673282236.0;
+__constant__ double d_kAE[4][4] = {
     {0, 0, 0, 0},
     {1767732205903.0 / 2027836641118.0, 0, 0, 0},
     {5535828885825.0 / 10492691773637.0, 788022342437.0 / 10882634858940.0, 0, 0},
     {6485989280629.0 / 16251701735622.0, -4246266847089.0 / 9704473918619.0,
      10755448449292.0 / 10357097424841.0, 0}};
-const double kAI[4][4] = {
+__constant__ double d_kAI[4][4] = {
     {0, 0, 0, 0},
     {1767732205903.0 / 4055673282236.0, 1767732205903.0 / 4055673282236.0, 0, 0},
     {2746238789719.0 / 10658868560708.0, -640167445237.0 / 6845629431997.0,
      1767732205903.0 / 4055673282236.0, 0},
     {1471266399579.0 / 7840856788654.0, -4482444167858.0 / 7529755066697.0,
      11266239266428.0 / 11593286722821.0, 1767732205903.0 / 4055673282236.0}};
-const double kB[4] = {1471266399579.0 / 7840856788654.0, -4482444167858.0 / 7529755066697.0,
-                      11266239266428.0 / 11593286722821.0, 1767732205903.0 / 4055673282236.0};
-const double kD[4] = {2756255671327.0 / 12835298489170.0, -10771552573575.0 / 22201958757719.0,
-                      9247589265047.0 / 10645013368117.0, 2193209047091.0 / 5459859503100.0};
+__constant__ double d_kB[4] = {1471266399579.0 / 7840856788654.0, -4482444167858.0 / 7529755066697.0,
+                               11266239266428.0 / 11593286722821.0, 1767732205903.0 / 4055673282236.0};
+__constant__ double d_kD[4] = {2756255671327.0 / 12835298489170.0, -10771552573575.0 / 22201958757719.0,
+                               9247589265047.0 / 10645013368117.0, 2193209047091.0 / 5459859503100.0};
 
 struct Geom {
   int dim, expl, has_y, has_z;
@@ -73,19 +75,179 @@ struct Geom {
   double kx, ky, kz, ks, lam_E;
 };
 
+// Device-resident controller state of one Evolve call (DESIGN R33): the
+// step size, time, current buffer, per-stage predicted iteration counts and
+// the statistics live here; the stage kernels read what they need at entry
+// and k_ark_control updates it after every round, so the host never waits
+// for a decision.  A round = the stages start..3 and the final combination
+// of one attempted step (start > 1: the stages of an attempt redone with a
+// corrected iteration count).
+struct ArkCtl {
+  double t, h;                  // time; step size (the current attempt's, clipped)
+  double h_unclipped;           // proposal before clipping to t_end
+  double t_end, tol_nl;
+  int clipped, cur;             // cur: y_n = ybuf[cur]
+  int start;                    // first stage of this round (1..4)
+  int Kr[4];                    // Newton iterations per stage in this round ([1..3])
+  int kpred[3];                 // the last accepted count per stage (prediction)
+  int done;                     // 0 running; 1 t_end reached; 2 max_steps; 3 h underflow; 4 internal
+  int maxnl, max_steps, fixed, rounds_att;
+  long long attempts, accepted, rej_err, rej_nl, newton_iters, setups, iters_att, rounds;
+};
+
+// The host loop of BW_ArkEvolve (ark.cu) for one attempted step: stop
+// conditions, clipping to t_end, the stage iteration predictions.
+__device__ void ark_begin_attempt(ArkCtl& C) {
+  if (!(C.t_end - C.t > 1e-12 * fmax(1.0, fabs(C.t_end)))) { C.done = 1; return; }
+  if (C.attempts++ >= C.max_steps) { C.done = 2; return; }
+  C.h_unclipped = C.h;
+  C.clipped = C.t + C.h > C.t_end;
+  if (C.clipped) C.h = C.t_end - C.t;
+  if (C.h < 1e-14 * (1.0 + C.t)) { C.done = 3; return; }
+  C.start = 1;
+  C.iters_att = 0;
+  C.rounds_att = 0;
+  for (int i = 1; i <= 3; ++i)
+    C.Kr[i] = C.kpred[i - 1] >= 1 && C.kpred[i - 1] <= C.maxnl ? C.kpred[i - 1] : C.maxnl;
+}
+
+// After a round: the oracle's stage decisions (R31 per stage: the first k
+// with ν_k <= tol_nl; a zero pivot or no convergence within maxnl fails the
+// attempt), then — once the attempt is complete — the error test and
+// step-size update of BW_ArkEvolve, and the next attempt's setup.
+__device__ void ark_control(ArkCtl& C, const double* res) {
+  if (C.done) return;
+  C.rounds++;
+  bool nl_fail = false;
+  int redo = 0;
+  for (int i = C.start; i <= 3 && !redo && !nl_fail; ++i) {
+    const double* r = res + (i - 1) * kCols;
+    if (r[0] != 0.0) {                           // zero pivot: no iterations, step recomputed
+      C.setups += i;
+      C.newton_iters += C.iters_att;
+      nl_fail = true;
+      break;
+    }
+    int kstar = 0;
+    for (int k = 1; k <= C.Kr[i] && !kstar; ++k)
+      if (r[k] <= C.tol_nl) kstar = k;
+    if (kstar == C.Kr[i]) {
+      C.iters_att += C.Kr[i];
+      C.kpred[i - 1] = C.Kr[i];
+      continue;
+    }
+    if (kstar > 0) {
+      C.Kr[i] = kstar;                           // converged earlier: redo from this stage
+    } else if (C.Kr[i] < C.maxnl) {
+      C.Kr[i] = C.maxnl;                         // not yet converged: redo with the maximum
+    } else {                                     // no convergence within maxnl
+      C.setups += i;
+      C.newton_iters += C.iters_att + C.maxnl;
+      C.kpred[i - 1] = C.maxnl;
+      nl_fail = true;
+      break;
+    }
+    redo = i;
+  }
+  if (!nl_fail && redo) {                        // the same attempt, stages redo..3 again
+    C.start = redo;
+    if (++C.rounds_att > 8) C.done = 4;          // unreachable (each stage redoes at most twice)
+    return;
+  }
+  if (nl_fail) {
+    C.rej_nl++;
+    C.h *= 0.25;
+  } else {
+    C.setups += 3;
+    C.newton_iters += C.iters_att;
+    double dsm = res[3 * kCols + 1];
+    double fac = dsm > 0.0 ? 0.9 * pow(dsm, -1.0 / 3.0) : 5.0;
+    if (C.fixed) { dsm = 0.0; fac = 1.0; }
+    if (dsm <= 1.0) {
+      C.cur ^= 1;
+      C.t += C.h;
+      C.accepted++;
+      C.h *= fmin(5.0, fmax(0.2, fac));
+      if (C.clipped) C.h = fmax(C.h, C.h_unclipped);
+    } else {
+      C.rej_err++;
+      C.h *= fmin(1.0, fmax(0.2, fac));
+    }
+  }
+  ark_begin_attempt(C);
+}
+
+// the host's view of ArkCtl::done after a round (mapped pinned memory)
+__device__ __forceinline__ void ark_publish(const ArkCtl& C, volatile int* host_done) {
+  *host_done = C.done;
+  __threadfence_system();
+}
+
 struct Args {
-  const double* y;              // y_n = Z_0
+  double* ybuf[2];              // y_n / y_{n+1} (ArkCtl::cur selects y_n)
   const double* Z[3];           // Z_1..Z_3
-  const double* below[4];       // per state: what sits under local cell/plane 0 (halo or own wrap)
-  double* out;                  // Z_i (stage) or y_{n+1} (final)
-  double cE[4], cI[4];          // stage: h aE_ij, h aI_ij;  final: h b_j, h b_j
-  double cErr[4];               // final: h (b_j - d_j)
+  const double* below0[2];      // what sits under local plane 0 of ybuf[b] (halo or own wrap)
+  const double* below[4];       // [1..3]: what sits under local plane 0 of Z_j ([0] unused)
+  double* zout;                 // stage i: Z_i
+  ArkCtl* ctl;
+  int stage;                    // 1..3, 4 = final
+  // P = 1, final: the fold of all stage sums and k_ark_control run in the
+  // launch's last CTA (no separate launches between rounds)
+  int control;
+  double* sums_all;             // [stage][kCols]
+  unsigned long long* first_all;
+  double* res;
+  double nglobal;
+  volatile int* host_done;
   double* partials;             // [grid][kCols]
   unsigned* counter;            // in-kernel fold (self-resetting)
   double* sums;                 // this launch's kCols local sums
   unsigned long long* first;    // first singular cell (1-based), this stage
+};
+
+// The round's values, resolved at kernel entry from *ctl into shared memory
+// (read where they are used rather than held in registers across the tile
+// loop: the kernels are register-bound at 5 CTAs per SM).
+struct RoundRT {
+  const double* y;              // y_n = Z_0
+  const double* below0;         // its plane under local plane 0
+  double* out;                  // Z_i (stage) or y_{n+1} (final)
+  double gamma, m21, c22;       // hγ̂, RN(-γ·0), 1 + γ/ε
+  double cc[12];                // [h aE_ij | h aI_ij | -] (stage), [h b_j | h b_j | h (b_j - d_j)] (final)
   int krt;                      // Newton iterations of this launch
 };
+
+// The round's parameters from the controller state: false if this launch
+// has nothing to do (Evolve finished, or a stage before the round's start).
+// h-dependent constants are formed here with the host's operations (γ = h·γ̂,
+// 1 + γ/ε, h·a_ij), so they carry the same bits the host would pass.
+// false if this launch has nothing to do (Evolve finished, or a stage
+// before the round's start); else R (shared) is filled — the caller
+// synchronises the CTA before the first use.
+template <int NS, bool FINAL>
+__device__ __forceinline__ bool ark_resolve(const Args& a, const FusedParams& p, RoundRT& R) {
+  static_assert(FINAL ? NS == 4 : (NS >= 1 && NS <= 3), "stage i reads i states");
+  const ArkCtl& C = *a.ctl;
+  if (C.done != 0 || NS < C.start) return false;
+  const int t = threadIdx.x;
+  const double h = C.h;
+  if (t == 0) {
+    const bool c1 = C.cur != 0;
+    R.y = c1 ? a.ybuf[1] : a.ybuf[0];
+    R.below0 = c1 ? a.below0[1] : a.below0[0];
+    R.out = FINAL ? (c1 ? a.ybuf[0] : a.ybuf[1]) : a.zout;
+    R.gamma = h * d_kG;
+    R.m21 = -R.gamma * 0.0;
+    R.c22 = 1.0 + R.gamma / p.eps;
+    R.krt = FINAL ? 1 : C.Kr[NS & 3];
+  }
+  if (t < 4) {
+    R.cc[t] = FINAL ? h * d_kB[t] : h * d_kAE[NS & 3][t];
+    R.cc[4 + t] = FINAL ? h * d_kB[t] : h * d_kAI[NS & 3][t];
+    R.cc[8 + t] = h * (d_kB[t] - d_kD[t]);
+  }
+  return true;
+}
 
 template <int KIND>
 __device__ __forceinline__ void implicit_rhs(const FusedParams& p, const double (&q)[3], double (&fi)[3]) {
@@ -100,29 +262,30 @@ __device__ __forceinline__ void implicit_rhs(const FusedParams& p, const double 
   fi[2] = __fma_rn(-w, u + p.rcp_eps, p.beps);                          // (B - w)/ε - wu
 }
 
-// Contracted modified Newton on one cell (R30 arithmetic, γ = p.gamma):
+// Contracted modified Newton on one cell (R30 arithmetic, γ = gam):
 // false (z untouched) if the Newton matrix needs a row exchange or a pivot
 // leaves the guarded range — the caller then runs newton_exact.
 template <int KIND>
-__device__ __forceinline__ bool newton_ct(const FusedParams& p, const double (&d)[3], double (&z)[3],
+__device__ __forceinline__ bool newton_ct(const FusedParams& p, const double gam, const double c22,
+                                          const double (&d)[3], double (&z)[3],
                                           const double (&ew)[3], int krt, double (&nu)[kMaxNL]) {
   double a00, a01, a02, a10, a11, a12, a20, a21, a22;
   if (KIND == 1) {
-    const double m = __fma_rn(-p.gamma, p.lam_I, 1.0);
+    const double m = __fma_rn(-gam, p.lam_I, 1.0);
     a00 = a11 = a22 = m;
     a01 = a02 = a10 = a12 = a20 = a21 = 0.0;
   } else {
     const double u = z[0], v = z[1], w = z[2];
-    const double uu = u * u, uv2 = (u + u) * v, gu = p.gamma * u;
-    a01 = -p.gamma * uu;
-    a00 = __fma_rn(-p.gamma, uv2 - (w + 1.0), 1.0);
+    const double uu = u * u, uv2 = (u + u) * v, gu = gam * u;
+    a01 = -gam * uu;
+    a00 = __fma_rn(-gam, uv2 - (w + 1.0), 1.0);
     a02 = gu;
-    a10 = p.gamma * (uv2 - w);
+    a10 = gam * (uv2 - w);
     a11 = 1.0 - a01;
     a12 = -gu;
-    a20 = p.gamma * w;
+    a20 = gam * w;
     a21 = 0.0;
-    a22 = p.c22 + gu;
+    a22 = c22 + gu;
   }
   bool ok = !mag_gt(a10, a00) & !mag_gt(a20, a00) & safe_mag(a00);
   const double p0 = rcp_nr2(a00);
@@ -143,9 +306,9 @@ __device__ __forceinline__ bool newton_ct(const FusedParams& p, const double (&d
     if (it >= krt) break;
     double f[3];
     implicit_rhs<KIND>(p, z, f);
-    double r0 = __fma_rn(p.gamma, f[0], d[0] - z[0]);
-    double r1 = __fma_rn(p.gamma, f[1], d[1] - z[1]);
-    double r2 = __fma_rn(p.gamma, f[2], d[2] - z[2]);
+    double r0 = __fma_rn(gam, f[0], d[0] - z[0]);
+    double r1 = __fma_rn(gam, f[1], d[1] - z[1]);
+    double r2 = __fma_rn(gam, f[2], d[2] - z[2]);
     r1 = __fma_rn(-l10, r0, r1);
     r2 = __fma_rn(-l21, r1, __fma_rn(-l20, r0, r2));
     r2 = r2 * p2;
@@ -161,45 +324,52 @@ __device__ __forceinline__ bool newton_ct(const FusedParams& p, const double (&d
 }
 
 // The same iteration with partial pivoting and IEEE divisions (the exact
-// primitives of the composed path); returns false for a zero pivot.
+// primitives of the composed path); returns false for a zero pivot.  Its
+// operands travel in one local record built only on this (rare) path, and
+// the parameters by value, so the fast path's arrays stay in registers.
+struct ExactIO {
+  double d[3], z[3], ew[3], nu[kMaxNL];
+};
 template <int KIND>
-__device__ __noinline__ bool newton_exact(const FusedParams& p, const double (&d)[3], double (&z)[3],
-                                          const double (&ew)[3], int krt, double (&nu)[kMaxNL]) {
+__device__ __noinline__ bool newton_exact(const FusedParams p, ExactIO& io, int krt) {
   double a[3][3], rp[3];
-  newton_matrix<KIND>(p, z, a);
+  newton_matrix<KIND>(p, io.z, a);
   bool singular = false;
   DivExact dv{true};
   const int code = lu3(a, rp, singular, dv);
   for (int it = 0; it < krt; ++it) {
     double f[3], r[3];
-    reaction<KIND>(p, z, f, dv);
+    reaction<KIND>(p, io.z, f, dv);
 #pragma unroll
-    for (int s = 0; s < 3; ++s) r[s] = __dadd_rn(__dadd_rn(d[s], __dmul_rn(p.gamma, f[s])), -z[s]);
+    for (int s = 0; s < 3; ++s) r[s] = __dadd_rn(__dadd_rn(io.d[s], __dmul_rn(p.gamma, f[s])), -io.z[s]);
     solve3(a, code, true, rp, r, dv);
     double w = 0.0;
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      z[s] = __dadd_rn(z[s], r[s]);
-      const double q = r[s] * ew[s];
+      io.z[s] = __dadd_rn(io.z[s], r[s]);
+      const double q = r[s] * io.ew[s];
       w = __fma_rn(q, q, w);
     }
-#pragma unroll
-    for (int k = 0; k < kMaxNL; ++k)
-      if (k == it) nu[k] += w;
+    io.nu[it] = w;
   }
   return !singular;
 }
 
-// One cell of a stage (or of the final combination) from its loaded
-// neighbourhood: ld(j, which, s) returns component s of state j at the cell
-// (which = 0), its x- (1), y- (2) and z-neighbour (3) upwind; the result
-// (Z_i or y_{n+1}) goes to o[3]; ν partials into nu.
+// One cell of a stage (or of the final combination), in two phases so that
+// the tiled kernel can release its input tiles between them:
+// ark_gather reads the cell's loaded neighbourhood — ld(j, which, s) returns
+// component s of state j at the cell (which = 0), its x- (1), y- (2) and
+// z-neighbour (3) upwind — and reduces it to the stage right-hand side d,
+// the predictor q = Z_{i-1} and ewt(y_n) (FINAL: the result o = y_{n+1} and
+// the error-norm partial); ark_solve then runs the stage's Newton iterations
+// on registers only.
 // FULL3D: the tiled kernels' geometry (upwind advection on all three axes)
 // known at compile time, no per-cell operator branches
 template <int NS, bool FINAL, int KIND, bool FULL3D, class Ld>
-__device__ __forceinline__ void ark_cell(const FusedParams& p, const Geom& g, const Args& a, const Ld& ld,
-                                         double (&o)[3], double (&nu)[kMaxNL], int64_t c) {
-  double yn[3], ew[3], acc[3] = {0.0, 0.0, 0.0}, err[3] = {0.0, 0.0, 0.0}, q[3];
+__device__ __forceinline__ void ark_gather(const FusedParams& p, const Geom& g, const RoundRT& R, const Ld& ld,
+                                           double (&d)[3], double (&q)[3], double (&ew)[3],
+                                           double (&nu)[kMaxNL]) {
+  double yn[3], acc[3] = {0.0, 0.0, 0.0}, err[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
     yn[s] = ld(0, 0, s);
@@ -228,41 +398,72 @@ __device__ __forceinline__ void ark_cell(const FusedParams& p, const Geom& g, co
     implicit_rhs<KIND>(p, q, fi);
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      acc[s] = __fma_rn(a.cE[j], fe[s], __fma_rn(a.cI[j], fi[s], acc[s]));
-      if (FINAL) err[s] = __fma_rn(a.cErr[j], fe[s] + fi[s], err[s]);
+      acc[s] = __fma_rn(R.cc[j], fe[s], __fma_rn(R.cc[4 + j], fi[s], acc[s]));
+      if (FINAL) err[s] = __fma_rn(R.cc[8 + j], fe[s] + fi[s], err[s]);
     }
   }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) d[s] = yn[s] + acc[s];                   // FINAL: y_{n+1}; stage: rhs
   if (FINAL) {
     double w = 0.0;
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      o[s] = yn[s] + acc[s];
       const double e = err[s] * ew[s];
       w = __fma_rn(e, e, w);
     }
     nu[0] += w;
-  } else {
-    double d[3];
+  }
+}
+
+// Newton on one stage cell from the predictor q; the stage value to o.
+template <int KIND>
+__device__ __forceinline__ void ark_solve(const FusedParams& p, const RoundRT& R, const Args& a, const double (&d)[3],
+                                          const double (&q)[3], const double (&ew)[3], double (&o)[3],
+                                          double (&nu)[kMaxNL], int64_t c) {
+#pragma unroll
+  for (int s = 0; s < 3; ++s) o[s] = q[s];                             // predictor Z_{i-1}
+  if (!newton_ct<KIND>(p, R.gamma, R.c22, d, o, ew, R.krt, nu)) {
+    ExactIO io;
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      d[s] = yn[s] + acc[s];
-      o[s] = q[s];                                                     // predictor Z_{i-1}
+      io.d[s] = d[s];
+      io.z[s] = q[s];
+      io.ew[s] = ew[s];
     }
-    if (!newton_ct<KIND>(p, d, o, ew, a.krt, nu)) {
+    FusedParams pe = p;
+    pe.gamma = R.gamma;
+    pe.m21 = R.m21;
+    pe.c22 = R.c22;
+    const bool ok = newton_exact<KIND>(pe, io, R.krt);
 #pragma unroll
-      for (int s = 0; s < 3; ++s) o[s] = q[s];
-      if (!newton_exact<KIND>(p, d, o, ew, a.krt, nu)) atomicMin(a.first, (unsigned long long)(c + 1));
-    }
+    for (int s = 0; s < 3; ++s) o[s] = io.z[s];
+#pragma unroll
+    for (int k = 0; k < kMaxNL; ++k)
+      if (k < R.krt) nu[k] += io.nu[k];
+    if (!ok) atomicMin(a.first, (unsigned long long)(c + 1));
+  }
+}
+
+template <int NS, bool FINAL, int KIND, bool FULL3D, class Ld>
+__device__ __forceinline__ void ark_cell(const FusedParams& p, const Geom& g, const RoundRT& R, const Args& a,
+                                         const Ld& ld, double (&o)[3], double (&nu)[kMaxNL], int64_t c) {
+  double d[3], q[3], ew[3];
+  ark_gather<NS, FINAL, KIND, FULL3D>(p, g, R, ld, d, q, ew, nu);
+  if (FINAL) {
+#pragma unroll
+    for (int s = 0; s < 3; ++s) o[s] = d[s];
+  } else {
+    ark_solve<KIND>(p, R, a, d, q, ew, o, nu, c);
   }
 }
 
 // CTA partials of nu (fixed order), then the last CTA to arrive folds every
 // CTA's row into a.sums (deterministic: lane-strided + shuffle tree)
 template <int NT>
-__device__ __forceinline__ void ark_epilogue(const Args& a, bool fin, double (&nu)[kMaxNL],
+__device__ __forceinline__ void ark_epilogue(const Args& a, bool fin, int krt, double (&nu)[kMaxNL],
                                              double (&red)[NT / 32][kCols], int& last) {
   const int t = threadIdx.x;
-  const int KC = fin ? 1 : a.krt;
+  const int KC = fin ? 1 : krt;
   const int w = t >> 5, l = t & 31;
 #pragma unroll
   for (int k = 0; k < kMaxNL; ++k) {
@@ -298,12 +499,28 @@ __device__ __forceinline__ void ark_epilogue(const Args& a, bool fin, double (&n
     if (l == 0) a.sums[col] = v;
   }
   if (t == 0) *a.counter = 0u;
+  if (!fin || !a.control) return;
+  __syncthreads();                             // this CTA's sums are visible to it
+  if (t < kStages * kCols) {                   // k_ark_pack_finalize
+    const int st = t / kCols;
+    a.res[t] = (t % kCols) == 0 ? (a.first_all[st] != ~0ull ? 1.0 : 0.0)
+                                : __dsqrt_rn(__ddiv_rn(__ldcg(a.sums_all + t), a.nglobal));
+  }
+  __syncthreads();
+  if (t < kStages) a.first_all[t] = ~0ull;
+  if (t == 0) {
+    ark_control(*a.ctl, a.res);
+    ark_publish(*a.ctl, a.host_done);
+  }
 }
 
 // Plain variant (any geometry): one thread per cell, grid-stride, loads
 // from global memory (neighbours through L1/L2).
 template <int NS, bool FINAL, int KIND>
 __global__ void __launch_bounds__(kThreads, 2) k_ark_stage(FusedParams p, Geom g, Args a) {
+  __shared__ RoundRT R;
+  if (!ark_resolve<NS, FINAL>(a, p, R)) return;
+  __syncthreads();
   __shared__ double red[kThreads / 32][kCols];
   __shared__ int last;
   double nu[kMaxNL];
@@ -313,8 +530,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_ark_stage(FusedParams p, Geom g
   for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < g.G; c += (int64_t)gridDim.x * kThreads) {
     const int64_t k = c / plane, rem = c - k * plane, jy = rem / g.nx, i = rem - jy * g.nx;
     auto ld = [&](int j, int which, int s) -> double {
-      const double* Zj = j == 0 ? a.y : a.Z[j - 1];
-      const double* b = a.below[j];
+      const double* Zj = j == 0 ? R.y : a.Z[j - 1];
+      const double* b = j == 0 ? R.below0 : a.below[j];
       switch (which) {
         case 0: return Zj[3 * c + s];
         case 1: return __ldg((i > 0 ? Zj + 3 * (c - 1) : (g.dim == 1 ? b : Zj + 3 * (c + g.nx - 1))) + s);
@@ -323,11 +540,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_ark_stage(FusedParams p, Geom g
       }
     };
     double o[3];
-    ark_cell<NS, FINAL, KIND, false>(p, g, a, ld, o, nu, c);
+    ark_cell<NS, FINAL, KIND, false>(p, g, R, a, ld, o, nu, c);
 #pragma unroll
-    for (int s = 0; s < 3; ++s) a.out[3 * c + s] = o[s];
+    for (int s = 0; s < 3; ++s) R.out[3 * c + s] = o[s];
   }
-  ark_epilogue<kThreads>(a, FINAL, nu, red, last);
+  ark_epilogue<kThreads>(a, FINAL, R.krt, nu, red, last);
 }
 
 // Tiled variant (3D upwind advection, nx % 128 == 0, both transverse axes
@@ -345,14 +562,20 @@ struct __align__(128) ArkTileSmem {
   double out[2][kTile * 3];
   uint64_t full[KS];
   double red[kTile / 32][kCols];
+  RoundRT rt;
   int last;
 };
 
-// KS: input stages in the shared ring (2: double-buffered; 1: more CTAs per SM)
-template <int NS, bool FINAL, int KIND, int KS>
+// KS: input stages in the shared ring (2: double-buffered; 1: more CTAs per
+// SM).  ER (early release): the input tiles are released — and the ring
+// slot refilled with the tile KS ahead — as soon as every thread has reduced
+// its neighbourhood to registers (ark_gather), so the copies run under the
+// stage's Newton iterations instead of after them.
+template <int NS, bool FINAL, int KIND, int KS, bool ER>
 __global__ void __launch_bounds__(kTile) k_ark_tile(FusedParams p, Geom g, Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   ArkTileSmem<NS, KS>& S = *reinterpret_cast<ArkTileSmem<NS, KS>*>(smem_raw);
+  RoundRT& R = S.rt;                                      // filled by ark_resolve below
   const int t = threadIdx.x;
   const int64_t ntiles = g.G / kTile, plane = g.nx * g.ny;
   constexpr uint32_t kTB = kTile * 3 * 8;
@@ -363,11 +586,11 @@ __global__ void __launch_bounds__(kTile) k_ark_tile(FusedParams p, Geom g, Args 
     sunbw::pipe::mbar_expect_tx(&S.full[st], NS * (3 * kTB + 48));
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
-      const double* Zj = j == 0 ? a.y : a.Z[j - 1];
+      const double* Zj = j == 0 ? R.y : a.Z[j - 1];
       sunbw::pipe::bulk_g2s(S.in[st][j][0], Zj + 3 * (int64_t)c0, kTB, &S.full[st]);
       sunbw::pipe::bulk_g2s(S.in[st][j][1], jr > 0 ? Zj + 3 * ((int64_t)c0 - g.nx) : Zj + 3 * ((int64_t)c0 + (g.ny - 1) * g.nx),
                      kTB, &S.full[st]);
-      sunbw::pipe::bulk_g2s(S.in[st][j][2], k > 0 ? Zj + 3 * ((int64_t)c0 - plane) : a.below[j] + 3 * ((int64_t)jr * g.nx + i0),
+      sunbw::pipe::bulk_g2s(S.in[st][j][2], k > 0 ? Zj + 3 * ((int64_t)c0 - plane) : (j == 0 ? R.below0 : a.below[j]) + 3 * ((int64_t)jr * g.nx + i0),
                      kTB, &S.full[st]);
       sunbw::pipe::bulk_g2s(S.xm[st][j], Zj + 3 * (xprev - 1), 48, &S.full[st]);
     }
@@ -376,6 +599,7 @@ __global__ void __launch_bounds__(kTile) k_ark_tile(FusedParams p, Geom g, Args 
     for (int st = 0; st < KS; ++st) sunbw::pipe::mbar_init(&S.full[st], 1);
     sunbw::pipe::fence_mbar_init();
   }
+  if (!ark_resolve<NS, FINAL>(a, p, R)) return;
   __syncthreads();
   if (t == 0)
     for (int st = 0; st < KS; ++st) {
@@ -388,6 +612,7 @@ __global__ void __launch_bounds__(kTile) k_ark_tile(FusedParams p, Geom g, Args 
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % KS, ob = it & 1;
+    const int64_t next = tile + KS * (int64_t)gridDim.x;
     sunbw::pipe::mbar_wait(&S.full[st], (uint32_t)((it / KS) & 1));
     const double* sb = &S.in[st][0][0][3 * t];        // this cell in the stage's tiles
     const double* sx = t > 0 ? &S.in[st][0][0][3 * (t - 1)] : &S.xm[st][0][3];
@@ -400,27 +625,37 @@ __global__ void __launch_bounds__(kTile) k_ark_tile(FusedParams p, Geom g, Args 
         default: return sb[j * (3 * kTile * 3) + 2 * kTile * 3 + s];
       }
     };
-    double o[3];
-    ark_cell<NS, FINAL, KIND, true>(p, g, a, ld, o, nu, tile * kTile + t);
+    double d[3], q[3], ew[3], o[3];
+    ark_gather<NS, FINAL, KIND, true>(p, g, R, ld, d, q, ew, nu);
+    if (ER) {
+      __syncthreads();                                 // every thread is done with in[st]
+      if (t == 0 && next < ntiles) issue(next, st);
+    }
+    if (FINAL) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) o[s] = d[s];
+    } else {
+      ark_solve<KIND>(p, R, a, d, q, ew, o, nu, tile * kTile + t);
+    }
 #pragma unroll
     for (int s = 0; s < 3; ++s) S.out[ob][3 * t + s] = o[s];
     sunbw::pipe::fence_async_smem();
     if (t == 0) sunbw::pipe::bulk_wait_read_all();          // out[ob] of two tiles ago has left
     __syncthreads();
     if (t == 0) {
-      sunbw::pipe::bulk_s2g(a.out + tile * (kTile * 3), S.out[ob], kTB);
+      sunbw::pipe::bulk_s2g(R.out + tile * (kTile * 3), S.out[ob], kTB);
       sunbw::pipe::bulk_commit();
-      const int64_t next = tile + KS * (int64_t)gridDim.x;
-      if (next < ntiles) issue(next, st);
+      if (!ER && next < ntiles) issue(next, st);
     }
   }
   if (t == 0) sunbw::pipe::bulk_wait_all();
-  ark_epilogue<kTile>(a, FINAL, nu, S.red, S.last);
+  ark_epilogue<kTile>(a, FINAL, R.krt, nu, S.red, S.last);
 }
 
 // flags (singular per stage, 0/1) into column 0 of each stage's sums, and
 // the singular records reset for the next round
-__global__ void k_ark_pack(unsigned long long* first, double* sums) {
+__global__ void k_ark_pack(const ArkCtl* C, unsigned long long* first, double* sums) {
+  if (C->done) return;
   const int s = threadIdx.x;
   if (s < kStages) {
     sums[s * kCols] = first[s] != ~0ull ? 1.0 : 0.0;
@@ -428,12 +663,24 @@ __global__ void k_ark_pack(unsigned long long* first, double* sums) {
   }
 }
 // (global) sums -> [flag, ν_1..ν_4] per stage; the final's column 1 = dsm
-__global__ void k_ark_finalize(const double* sums, double nglobal, double* res) {
+__global__ void k_ark_finalize(const ArkCtl* C, const double* sums, double nglobal, double* res) {
+  if (C->done) return;
   const int t = threadIdx.x;
   if (t < kStages * kCols) res[t] = (t % kCols) == 0 ? sums[t] : __dsqrt_rn(__ddiv_rn(sums[t], nglobal));
 }
+__global__ void k_ark_begin(ArkCtl* C, volatile int* host_done) {
+  ark_begin_attempt(*C);
+  ark_publish(*C, host_done);
+}
+__global__ void k_ark_control(ArkCtl* C, const double* res, volatile int* host_done) {
+  ark_control(*C, res);
+  ark_publish(*C, host_done);
+}
+
 // one rank: both in one launch
-__global__ void k_ark_pack_finalize(unsigned long long* first, double nglobal, double* res, double* sums) {
+__global__ void k_ark_pack_finalize(const ArkCtl* C, unsigned long long* first, double nglobal, double* res,
+                                    double* sums) {
+  if (C->done) return;
   const int t = threadIdx.x;
   if (t < kStages * kCols) {
     const int st = t / kCols;
@@ -456,18 +703,23 @@ struct ArkFused {
   ArkGeometry geo;
   int64_t nglobal;
   double* Z[3] = {};
-  double* halo[4] = {};          // P > 1: the left neighbour's last plane of each state
+  double* halo[4] = {};          // P > 1: the left neighbour's last plane of Z_1..Z_3 ([1..3])
+  double* halo0[2] = {};         // P > 1: ... of each y buffer
   double* partials = nullptr;
   double* sums = nullptr;        // [stage 0..3][kCols] (stage 3 = final)
   double* res = nullptr;
   unsigned* counter = nullptr;
   unsigned long long* first = nullptr;
-  double* h_res = nullptr;       // pinned
+  ArkCtl* ctl = nullptr;         // device controller state
+  ArkCtl* h_ctl = nullptr;       // pinned staging for the controller state
+  int* h_done = nullptr;         // mapped pinned: ArkCtl::done after the latest round
+  int* d_done = nullptr;         // ... its device address
+  cudaEvent_t ev[2] = {};
   int kpred[3] = {0, 0, 0};
   int grid = 1;                  // plain kernels
   bool tiled = false;            // 3D upwind, nx % 128 == 0: the TMA-tiled kernels
   int tgrid[5] = {};             // tiled kernels' persistent grid per NS (1..4)
-  int tgrid_ks[5] = {};          // ... computed for this ring depth
+  int tgrid_ks[5] = {};          // ... computed for this ring configuration
 };
 
 ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal) {
@@ -481,8 +733,10 @@ ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal) {
   F->grid = (int)(need < 1 ? 1 : (need < cap ? need : cap));
   bool ok = true;
   for (auto& z : F->Z) ok = ok && cudaMalloc(&z, sizeof(double) * n) == cudaSuccess;
-  if (ctx_nranks(ctx) > 1)
-    for (auto& hb : F->halo) ok = ok && cudaMalloc(&hb, sizeof(double) * F->geo.halo_len) == cudaSuccess;
+  if (ctx_nranks(ctx) > 1) {
+    for (int j = 1; j < 4; ++j) ok = ok && cudaMalloc(&F->halo[j], sizeof(double) * F->geo.halo_len) == cudaSuccess;
+    for (auto& hb : F->halo0) ok = ok && cudaMalloc(&hb, sizeof(double) * F->geo.halo_len) == cudaSuccess;
+  }
   const ArkGeometry& g = F->geo;
   F->tiled = g.dim == 3 && g.expl == 0 && g.has_y && g.has_z && g.nx % kTile == 0 && g.G % kTile == 0 &&
              g.G > 0 && g.G < (int64_t(1) << 31);
@@ -491,7 +745,12 @@ ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal) {
        cudaMalloc(&F->res, sizeof(double) * kStages * kCols) == cudaSuccess &&
        cudaMalloc(&F->counter, sizeof(unsigned)) == cudaSuccess &&
        cudaMalloc(&F->first, sizeof(unsigned long long) * kStages) == cudaSuccess &&
-       cudaHostAlloc(&F->h_res, sizeof(double) * kStages * kCols, cudaHostAllocDefault) == cudaSuccess &&
+       cudaMalloc(&F->ctl, sizeof(ArkCtl)) == cudaSuccess &&
+       cudaHostAlloc(&F->h_ctl, sizeof(ArkCtl), cudaHostAllocDefault) == cudaSuccess &&
+       cudaHostAlloc(&F->h_done, sizeof(int), cudaHostAllocMapped) == cudaSuccess &&
+       cudaHostGetDevicePointer((void**)&F->d_done, F->h_done, 0) == cudaSuccess &&
+       cudaEventCreateWithFlags(&F->ev[0], cudaEventDisableTiming) == cudaSuccess &&
+       cudaEventCreateWithFlags(&F->ev[1], cudaEventDisableTiming) == cudaSuccess &&
        cudaMemsetAsync(F->counter, 0, sizeof(unsigned), ctx->stream) == cudaSuccess &&
        cudaMemsetAsync(F->first, 0xFF, sizeof(unsigned long long) * kStages, ctx->stream) == cudaSuccess;
   if (!ok) {
@@ -508,49 +767,67 @@ void ark_fused_destroy(ArkFused* F) {
     if (z) cudaFree(z);
   for (auto hb : F->halo)
     if (hb) cudaFree(hb);
+  for (auto hb : F->halo0)
+    if (hb) cudaFree(hb);
   if (F->partials) cudaFree(F->partials);
   if (F->sums) cudaFree(F->sums);
   if (F->res) cudaFree(F->res);
   if (F->counter) cudaFree(F->counter);
   if (F->first) cudaFree(F->first);
-  if (F->h_res) cudaFreeHost(F->h_res);
+  if (F->ctl) cudaFree(F->ctl);
+  if (F->h_ctl) cudaFreeHost(F->h_ctl);
+  if (F->h_done) cudaFreeHost(F->h_done);
+  for (auto e : F->ev)
+    if (e) cudaEventDestroy(e);
   delete F;
 }
 
 namespace {
 
-template <int NS, bool FINAL, int KIND, int KS>
+template <class Kern>
+int launch_ark(Kern fn, int grid, int block, int smem, cudaStream_t s, const FusedParams& p, const Geom& g,
+               const Args& a) {
+  fn<<<grid, block, smem, s>>>(p, g, a);
+  return 0;
+}
+
+template <int NS, bool FINAL, int KIND, int KS, bool ER>
 int launch_tiled_ks(ArkFused* F, const FusedParams& p, const Geom& g, const Args& a) {
   const int bytes = (int)sizeof(ArkTileSmem<NS, KS>);
-  auto fn = k_ark_tile<NS, FINAL, KIND, KS>;
+  auto fn = k_ark_tile<NS, FINAL, KIND, KS, ER>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
     return SUNBW_ERR_CUDA;
-  if (F->tgrid_ks[NS] != KS) {
+  const int cfg = KS * 2 + (ER ? 1 : 0);
+  if (F->tgrid_ks[NS] != cfg) {
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTile, bytes) != cudaSuccess || occ < 1)
       return SUNBW_ERR_CUDA;
     const int64_t ntiles = g.G / kTile, cap = (int64_t)F->ctx->nsm * (occ < 16 ? occ : 16);
     F->tgrid[NS] = (int)(ntiles < cap ? ntiles : cap);
-    F->tgrid_ks[NS] = KS;
+    F->tgrid_ks[NS] = cfg;
   }
-  fn<<<F->tgrid[NS], kTile, bytes, F->ctx->stream>>>(p, g, a);
-  return 0;
+  return launch_ark(fn, F->tgrid[NS], kTile, bytes, F->ctx->stream, p, g, a);
 }
 
-// stages per ring: SUNBW_ARK_KS (1 or 2) overrides, for A/B measurements
-int ark_ks(int NS) {
-  static const int ov = [] {
-    const char* e = std::getenv("SUNBW_ARK_KS");
-    return e ? std::atoi(e) : 0;
-  }();
-  (void)NS;
-  return ov == 1 || ov == 2 ? ov : 1;   // measured: single-buffered rings (more CTAs per SM) are faster
+// ring configuration per stage kind (NS = 1..3 stages, 4 = final):
+// SUNBW_ARK_CFG = four digits, one per NS, each 1 = (KS 1), 2 = (KS 2),
+// 3 = (KS 1, early release), 4 = (KS 2, early release) — for A/B runs
+int ark_cfg(int NS) {
+  static const char* ov = std::getenv("SUNBW_ARK_CFG");
+  static const char kDefault[] = "3331";
+  const char* c = ov && std::strlen(ov) == 4 ? ov : kDefault;
+  const int v = c[NS - 1] - '0';
+  return v >= 1 && v <= 4 ? v : 1;
 }
 
 template <int NS, bool FINAL, int KIND>
 int launch_tiled(ArkFused* F, const FusedParams& p, const Geom& g, const Args& a) {
-  return ark_ks(NS) == 1 ? launch_tiled_ks<NS, FINAL, KIND, 1>(F, p, g, a)
-                         : launch_tiled_ks<NS, FINAL, KIND, 2>(F, p, g, a);
+  switch (ark_cfg(NS)) {
+    case 2: return launch_tiled_ks<NS, FINAL, KIND, 2, false>(F, p, g, a);
+    case 3: return launch_tiled_ks<NS, FINAL, KIND, 1, true>(F, p, g, a);
+    case 4: return launch_tiled_ks<NS, FINAL, KIND, 2, true>(F, p, g, a);
+    default: return launch_tiled_ks<NS, FINAL, KIND, 1, false>(F, p, g, a);
+  }
 }
 
 template <int KIND>
@@ -563,134 +840,139 @@ int launch_stage(ArkFused* F, int NS, bool fin, const FusedParams& p, const Geom
     return launch_tiled<3, false, KIND>(F, p, g, a);
   }
   if (fin) {
-    k_ark_stage<4, true, KIND><<<F->grid, kThreads, 0, s>>>(p, g, a);
+    return launch_ark(k_ark_stage<4, true, KIND>, F->grid, kThreads, 0, s, p, g, a);
   } else if (NS == 1) {
-    k_ark_stage<1, false, KIND><<<F->grid, kThreads, 0, s>>>(p, g, a);
+    return launch_ark(k_ark_stage<1, false, KIND>, F->grid, kThreads, 0, s, p, g, a);
   } else if (NS == 2) {
-    k_ark_stage<2, false, KIND><<<F->grid, kThreads, 0, s>>>(p, g, a);
+    return launch_ark(k_ark_stage<2, false, KIND>, F->grid, kThreads, 0, s, p, g, a);
   } else {
-    k_ark_stage<3, false, KIND><<<F->grid, kThreads, 0, s>>>(p, g, a);
+    return launch_ark(k_ark_stage<3, false, KIND>, F->grid, kThreads, 0, s, p, g, a);
   }
   return 0;
 }
 
 }  // namespace
 
-// One attempted step of size h from y (y_{n+1} -> ynew).  *nl_ok = 0 if a
-// stage solve failed (zero pivot, or no convergence within maxnl): the
-// caller recomputes with h/4.  newton_iters / setups: the oracle's counts
-// for this attempt (stages reached, iterations performed).
-int ark_fused_attempt(ArkFused* F, const double* y, double* ynew, double h, double rtol, double atol,
-                      double tol_nl, int maxnl, int* nl_ok, double* dsm, int64_t* newton_iters,
-                      int64_t* setups) {
+// BW_ArkEvolve's loop for the fused stages, driven from the device
+// (DESIGN R33): every round — the stage kernels, the final combination, the
+// fold (+ allreduce at P > 1) and k_ark_control — is enqueued without
+// waiting for the previous one's decision; each kernel reads the round's
+// h, current buffer, start stage and iteration counts from ArkCtl and exits
+// at once if it has nothing to do.  At P = 1 a round is the four stage
+// launches alone (the final launch's last CTA folds the norms and runs the
+// controller).  The controller publishes ArkCtl::done to mapped pinned
+// memory; the host keeps two rounds in flight, waits for the older one's
+// event and reads the flag to know when the Evolve call has finished (at
+// most one no-op round follows).
+// *y / *ynew are swapped if the result ended in the second buffer.
+int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* h, double t_end,
+                     const BW_ArkOptions& opt, BW_ArkStats* st, int* rc) {
   SUNBW_Context ctx = F->ctx;
-  if (maxnl < 1 || maxnl > kMaxNL) return ctx_set_err(ctx, SUNBW_ERR_ARG);
+  if (opt.maxnl < 1 || opt.maxnl > kMaxNL) return ctx_set_err(ctx, SUNBW_ERR_ARG);
   const ArkGeometry& G0 = F->geo;
   const bool multi = ctx_nranks(ctx) > 1;
-  FusedParams p = fused_params(bw_params(F->prob), false, h, rtol, atol);
-  p.gamma = h * kG;
-  p.m21 = -p.gamma * 0.0;
-  p.c22 = 1.0 + p.gamma / p.eps;
-  Geom g{G0.dim, G0.expl, G0.has_y, G0.has_z, G0.nx, G0.ny, G0.nzl, G0.G, G0.kx, G0.ky, G0.kz,
-         G0.kx + (G0.has_y ? G0.ky : 0.0) + (G0.has_z ? G0.kz : 0.0), G0.lam_E};
-  const double* states[4] = {y, F->Z[0], F->Z[1], F->Z[2]};
-  auto below = [&](int j) -> const double* {
-    return multi ? F->halo[j] : states[j] + 3 * G0.G - G0.halo_len;
-  };
-  auto exchange = [&](int j) -> int {           // halo of state j (P > 1; advection only)
+  cudaStream_t s = ctx->stream;
+  const FusedParams p = fused_params(bw_params(F->prob), false, 0.0, opt.rtol, opt.atol);  // γ, c22: per round
+  const Geom g{G0.dim, G0.expl, G0.has_y, G0.has_z, G0.nx, G0.ny, G0.nzl, G0.G, G0.kx, G0.ky, G0.kz,
+               G0.kx + (G0.has_y ? G0.ky : 0.0) + (G0.has_z ? G0.kz : 0.0), G0.lam_E};
+  double* yb[2] = {*y, *ynew};
+  auto wrap = [&](const double* v) { return v + 3 * G0.G - G0.halo_len; };
+  ArkCtl& c = *F->h_ctl;
+  std::memset(&c, 0, sizeof(c));
+  c.t = *t;
+  c.h = *h;
+  c.t_end = t_end;
+  c.tol_nl = opt.tol_nl;
+  c.maxnl = opt.maxnl;
+  c.max_steps = opt.max_steps;
+  c.fixed = opt.fixed;
+  for (int i = 0; i < 3; ++i) c.kpred[i] = F->kpred[i];
+  if (cudaMemcpyAsync(F->ctl, &c, sizeof(ArkCtl), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  *(volatile int*)F->h_done = 0;
+  k_ark_begin<<<1, 1, 0, s>>>(F->ctl, F->d_done);
+  ctx->launches++;
+  Args base{};
+  for (int b = 0; b < 2; ++b) {
+    base.ybuf[b] = yb[b];
+    base.below0[b] = multi ? F->halo0[b] : wrap(yb[b]);
+  }
+  for (int j = 0; j < 3; ++j) {
+    base.Z[j] = F->Z[j];
+    base.below[j + 1] = multi ? F->halo[j + 1] : wrap(F->Z[j]);
+  }
+  base.ctl = F->ctl;
+  base.partials = F->partials;
+  base.counter = F->counter;
+  base.control = multi ? 0 : 1;
+  base.sums_all = F->sums;
+  base.first_all = F->first;
+  base.res = F->res;
+  base.nglobal = (double)F->nglobal;
+  base.host_done = F->d_done;
+  const bool kind1 = bw_params(F->prob).kind == 1;
+  auto exchange = [&](const double* v, double* dst) -> int {   // P > 1, advection only
     if (!multi || G0.expl != 0) return 0;
-    return ctx->comm->halo_shift(states[j] + 3 * G0.G - G0.halo_len, F->halo[j], (size_t)G0.halo_len,
-                                 ctx->stream);
+    return ctx->comm->halo_shift(wrap(v), dst, (size_t)G0.halo_len, s);
   };
-  int Kr[4] = {0, 0, 0, 0};
-  for (int i = 1; i <= 3; ++i) Kr[i] = F->kpred[i - 1] >= 1 && F->kpred[i - 1] <= maxnl ? F->kpred[i - 1] : maxnl;
-  if (int e = exchange(0)) return ctx_set_err(ctx, e);
-  int start = 1;
-  int64_t iters = 0;                             // iterations of the stages already accepted (< start)
-  for (int round = 0; round < 8; ++round) {
-    // (the singular records were reset by the previous round's pack; the
-    // stage sums are overwritten by each launch's fold)
-    for (int i = start; i <= 4; ++i) {           // stages start..3, then the final combination (i = 4)
+  auto round = [&]() -> int {
+    for (int b = 0; b < 2; ++b)
+      if (int e = exchange(yb[b], F->halo0[b])) return e;
+    for (int i = 1; i <= 4; ++i) {
       const bool fin = i == 4;
-      Args a{};
-      a.y = y;
-      for (int j = 0; j < 3; ++j) a.Z[j] = F->Z[j];
-      for (int j = 0; j < 4; ++j) a.below[j] = below(j);
-      a.out = fin ? ynew : F->Z[i - 1];
-      for (int j = 0; j < 4; ++j) {
-        a.cE[j] = fin ? h * kB[j] : h * kAE[i][j];
-        a.cI[j] = fin ? h * kB[j] : h * kAI[i][j];
-        a.cErr[j] = h * (kB[j] - kD[j]);
-      }
-      a.partials = F->partials;
-      a.counter = F->counter;
+      Args a = base;
+      a.stage = i;
+      a.zout = fin ? nullptr : F->Z[i - 1];
       a.sums = F->sums + (i - 1) * kCols;
       a.first = F->first + (i - 1);
-      a.krt = fin ? 1 : Kr[i];
       if (G0.G > 0) {
-        const int e = bw_params(F->prob).kind == 1 ? launch_stage<1>(F, i, fin, p, g, a)
-                                                   : launch_stage<0>(F, i, fin, p, g, a);
-        if (e) return ctx_set_err(ctx, e);
+        const int e = kind1 ? launch_stage<1>(F, i, fin, p, g, a) : launch_stage<0>(F, i, fin, p, g, a);
+        if (e) return e;
         ctx->launches++;
         if (ctx_check_launch(ctx)) return SUNBW_ERR_CUDA;
       }
       if (!fin)
-        if (int e = exchange(i)) return ctx_set_err(ctx, e);
+        if (int e = exchange(F->Z[i - 1], F->halo[i])) return e;
     }
     if (multi) {
-      k_ark_pack<<<1, 32, 0, ctx->stream>>>(F->first, F->sums);
-      if (int e = ctx->comm->allreduce(F->sums, kStages * kCols, RED_SUM, ctx->stream)) return ctx_set_err(ctx, e);
-      k_ark_finalize<<<1, 32, 0, ctx->stream>>>(F->sums, (double)F->nglobal, F->res);
+      k_ark_pack<<<1, 32, 0, s>>>(F->ctl, F->first, F->sums);
+      if (int e = ctx->comm->allreduce(F->sums, kStages * kCols, RED_SUM, s)) return e;
+      k_ark_finalize<<<1, 32, 0, s>>>(F->ctl, F->sums, (double)F->nglobal, F->res);
+      k_ark_control<<<1, 1, 0, s>>>(F->ctl, F->res, F->d_done);
+      ctx->launches += 3;
+    } else if (G0.G == 0) {                      // (no final launch to carry the controller)
+      k_ark_pack_finalize<<<1, 32, 0, s>>>(F->ctl, F->first, (double)F->nglobal, F->res, F->sums);
+      k_ark_control<<<1, 1, 0, s>>>(F->ctl, F->res, F->d_done);
       ctx->launches += 2;
-    } else {
-      k_ark_pack_finalize<<<1, 32, 0, ctx->stream>>>(F->first, (double)F->nglobal, F->res, F->sums);
-      ctx->launches++;
     }
-    if (cudaMemcpyAsync(F->h_res, F->res, sizeof(double) * kStages * kCols, cudaMemcpyDeviceToHost,
-                        ctx->stream) != cudaSuccess ||
-        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
-      return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-    // the oracle's decisions, stage by stage, from the first recomputed one
-    int redo = 0;
-    for (int i = start; i <= 3 && !redo; ++i) {
-      const double* r = F->h_res + (i - 1) * kCols;
-      if (r[0] != 0.0) {                         // zero pivot: no iterations, step recomputed
-        *setups += i;
-        *newton_iters += iters;
-        *nl_ok = 0;
-        return 0;
-      }
-      int kstar = 0;
-      for (int k = 1; k <= Kr[i] && !kstar; ++k)
-        if (r[k] <= tol_nl) kstar = k;
-      if (kstar == Kr[i]) {
-        iters += Kr[i];
-        F->kpred[i - 1] = Kr[i];
-        continue;
-      }
-      if (kstar > 0) {
-        Kr[i] = kstar;                           // converged earlier: redo from this stage
-      } else if (Kr[i] < maxnl) {
-        Kr[i] = maxnl;                           // not yet converged: redo with the maximum
-      } else {                                   // no convergence within maxnl
-        *setups += i;
-        *newton_iters += iters + maxnl;
-        F->kpred[i - 1] = maxnl;
-        *nl_ok = 0;
-        return 0;
-      }
-      redo = i;
+    return cudaGetLastError() == cudaSuccess ? 0 : SUNBW_ERR_CUDA;
+  };
+  // each attempt takes at most 9 rounds (stages redone at most twice each)
+  const int64_t max_rounds = 9 * ((int64_t)opt.max_steps + 1) + 2;
+  for (int64_t k = 0;; ++k) {
+    if (k > max_rounds) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    if (int e = round()) return ctx_set_err(ctx, e);
+    if (cudaEventRecord(F->ev[k & 1], s) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    if (k > 0) {
+      if (cudaEventSynchronize(F->ev[(k - 1) & 1]) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      if (*(volatile int*)F->h_done) break;
     }
-    if (!redo) {
-      *setups += 3;
-      *newton_iters += iters;
-      *nl_ok = 1;
-      *dsm = F->h_res[3 * kCols + 1];
-      return 0;
-    }
-    start = redo;
   }
-  return ctx_set_err(ctx, SUNBW_ERR_CUDA);       // unreachable (each stage redoes at most twice)
+  if (cudaMemcpyAsync(&c, F->ctl, sizeof(ArkCtl), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  if (c.done == 4) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  *rc = c.done == 2 ? 1 : c.done == 3 ? 2 : 0;
+  *t = c.t;
+  *h = c.h;
+  if (c.cur) std::swap(*y, *ynew);
+  for (int i = 0; i < 3; ++i) F->kpred[i] = c.kpred[i];
+  st->accepted += c.accepted;
+  st->rejected_err += c.rej_err;
+  st->rejected_nl += c.rej_nl;
+  st->newton_iters += c.newton_iters;
+  st->setups += c.setups;
+  return 0;
 }
 
 }  // namespace sunbw

@@ -220,13 +220,12 @@ struct ArkGeometry {
   double kx, ky, kz, lam_E;
 };
 void bw_ark_geometry(void* prob, ArkGeometry* g);
-// one attempted ARK step on the device (ark_fused.cu); see the definition
+// the fused ARK stages and their device-driven Evolve loop (ark_fused.cu)
 struct ArkFused;
 ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal);
 void ark_fused_destroy(ArkFused* F);
-int ark_fused_attempt(ArkFused* F, const double* y, double* ynew, double h, double rtol, double atol,
-                      double tol_nl, int maxnl, int* nl_ok, double* dsm, int64_t* newton_iters,
-                      int64_t* setups);
+int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* h, double t_end,
+                     const BW_ArkOptions& opt, BW_ArkStats* st, int* rc);
 
 struct FusedFold {
   int prev_parts;            // partial rows written by earlier launches of this step

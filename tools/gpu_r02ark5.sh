@@ -1,0 +1,11 @@
+timeout 900 python -m pytest tests/test_gpu_ark.py tests/test_gpu_multirank_flags.py -q -p no:cacheprovider -x 2>&1 | tail -4
+for pdl in 1 0; do for cfg in 3331 3333; do
+  SUNBW_ARK_PDL=$pdl SUNBW_ARK_CFG=$cfg timeout 300 python tools/ark_timeline.py > gpurun_out/ark_tl_$cfg.json 2>gpurun_out/ark_tl_$cfg.err
+  python - $cfg $pdl <<'PY'
+import json,sys
+d=json.load(open(f"gpurun_out/ark_tl_{sys.argv[1]}.json"))
+print("pdl", sys.argv[2], sys.argv[1], d["span_us"], d["us_per_attempt"], d["stats"]["newton_iters"], {k:(v["count"],v["us_avg"]) for k,v in d["kernels"].items()})
+print("  gaps", {k:(v["count"],v["us_avg"]) for k,v in list(d["gaps"].items())[:6]})
+PY
+  SUNBW_ARK_PDL=$pdl SUNBW_ARK_CFG=$cfg timeout 300 python tools/ark_bench.py
+done; done
