@@ -715,6 +715,10 @@ struct ArkFused {
   int* h_done = nullptr;         // mapped pinned: ArkCtl::done after the latest round
   int* d_done = nullptr;         // ... its device address
   cudaEvent_t ev[2] = {};
+  cudaStream_t cap = nullptr;    // P = 1: one round captured as a graph (per y buffer pair)
+  cudaGraphExec_t gexec = nullptr;
+  const double* gkey[2] = {};
+  int64_t glaunches = 0;
   int kpred[3] = {0, 0, 0};
   int grid = 1;                  // plain kernels
   bool tiled = false;            // 3D upwind, nx % 128 == 0: the TMA-tiled kernels
@@ -779,6 +783,8 @@ void ark_fused_destroy(ArkFused* F) {
   if (F->h_done) cudaFreeHost(F->h_done);
   for (auto e : F->ev)
     if (e) cudaEventDestroy(e);
+  if (F->gexec) cudaGraphExecDestroy(F->gexec);
+  if (F->cap) cudaStreamDestroy(F->cap);
   delete F;
 }
 
@@ -814,7 +820,7 @@ int launch_tiled_ks(ArkFused* F, const FusedParams& p, const Geom& g, const Args
 // 3 = (KS 1, early release), 4 = (KS 2, early release) — for A/B runs
 int ark_cfg(int NS) {
   static const char* ov = std::getenv("SUNBW_ARK_CFG");
-  static const char kDefault[] = "3331";
+  static const char kDefault[] = "3333";      // measured (r02 ARK A/B, DESIGN R33)
   const char* c = ov && std::strlen(ov) == 4 ? ov : kDefault;
   const int v = c[NS - 1] - '0';
   return v >= 1 && v <= 4 ? v : 1;
@@ -871,7 +877,7 @@ int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* 
   if (opt.maxnl < 1 || opt.maxnl > kMaxNL) return ctx_set_err(ctx, SUNBW_ERR_ARG);
   const ArkGeometry& G0 = F->geo;
   const bool multi = ctx_nranks(ctx) > 1;
-  cudaStream_t s = ctx->stream;
+  cudaStream_t s = ctx->stream;                  // (switched to the capture stream while capturing)
   const FusedParams p = fused_params(bw_params(F->prob), false, 0.0, opt.rtol, opt.atol);  // γ, c22: per round
   const Geom g{G0.dim, G0.expl, G0.has_y, G0.has_z, G0.nx, G0.ny, G0.nzl, G0.G, G0.kx, G0.ky, G0.kz,
                G0.kx + (G0.has_y ? G0.ky : 0.0) + (G0.has_z ? G0.kz : 0.0), G0.lam_E};
@@ -947,11 +953,48 @@ int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* 
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SUNBW_ERR_CUDA;
   };
+  // P = 1: the round's four launches replayed from a graph (the kernels take
+  // everything that changes between rounds from ArkCtl)
+  const bool use_graph = !multi && G0.G > 0;
+  if (use_graph && (!F->gexec || F->gkey[0] != yb[0] || F->gkey[1] != yb[1])) {
+    if (F->gexec) cudaGraphExecDestroy(F->gexec);
+    F->gexec = nullptr;
+    if (!F->cap && cudaStreamCreateWithFlags(&F->cap, cudaStreamNonBlocking) != cudaSuccess)
+      return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    cudaStream_t user = ctx->stream;
+    const int64_t l0 = ctx->launches.load();
+    cudaGraph_t gr = nullptr;
+    int rc0 = 0;
+    ctx->stream = s = F->cap;
+    if (cudaStreamBeginCapture(F->cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      rc0 = SUNBW_ERR_CUDA;
+    } else {
+      rc0 = round();
+      if (cudaStreamEndCapture(F->cap, &gr) != cudaSuccess && !rc0) rc0 = SUNBW_ERR_CUDA;
+    }
+    ctx->stream = s = user;
+    F->glaunches = ctx->launches.load() - l0;
+    ctx->launches -= F->glaunches;
+    if (!rc0 && cudaGraphInstantiate(&F->gexec, gr, 0) != cudaSuccess) rc0 = SUNBW_ERR_CUDA;
+    if (gr) cudaGraphDestroy(gr);
+    if (rc0) {
+      cudaGetLastError();
+      F->gexec = nullptr;
+      return ctx_set_err(ctx, rc0 < 0 ? rc0 : SUNBW_ERR_CUDA);
+    }
+    F->gkey[0] = yb[0];
+    F->gkey[1] = yb[1];
+  }
   // each attempt takes at most 9 rounds (stages redone at most twice each)
   const int64_t max_rounds = 9 * ((int64_t)opt.max_steps + 1) + 2;
   for (int64_t k = 0;; ++k) {
     if (k > max_rounds) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-    if (int e = round()) return ctx_set_err(ctx, e);
+    if (use_graph) {
+      if (cudaGraphLaunch(F->gexec, s) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      ctx->launches += F->glaunches;
+    } else if (int e = round()) {
+      return ctx_set_err(ctx, e);
+    }
     if (cudaEventRecord(F->ev[k & 1], s) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
     if (k > 0) {
       if (cudaEventSynchronize(F->ev[(k - 1) & 1]) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
