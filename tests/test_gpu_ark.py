@@ -129,3 +129,40 @@ def test_ark_fused_multirank(S, shape):
         assert res[0][3][key] == res[1][3][key] == st2[key], key
     y = np.concatenate([r[2] for r in sorted(res, key=lambda t: t[1])])
     assert rel(y, yref) <= 1e-9
+
+
+@pytest.mark.parametrize("shape", [(128, 16, 8), (24, 10, 8)])
+def test_ark_fused_successive_evolve_calls(S, ctx, shape):
+    """The device-driven loop (DESIGN R33) across several Evolve calls on one
+    Ark object: t, h and the stage-count predictions carry over, the result
+    buffer may have swapped (the P = 1 round graph is re-captured for the new
+    pair), and a call whose t_end is already reached does no attempt.  The
+    composed path (host decisions) gives the same counts and, to the
+    north star's 1e-9, the same states after every call."""
+    nx, ny, nz = shape
+    y0 = oracle.bruss_ic(nx, ny, nz)
+    params = S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz)
+    P = S.Problem(ctx, params)
+    runs = {}
+    for fused in (False, True):
+        yd = torch.from_numpy(y0).cuda()
+        A = S.Ark(P, S.NVector(ctx, yd), h0=1e-4, fused=fused)
+        seq = []
+        for t_end in (0.001, 0.0015, 0.0015, 0.004):
+            yout = torch.empty_like(yd)
+            rc, st = A.evolve(t_end, S.NVector(ctx, yout))
+            assert rc == 0
+            seq.append((dict(st), yout.cpu().numpy()))
+        A.destroy()
+        runs[fused] = seq
+    P.destroy()
+    for (sc, yc), (sf, yf) in zip(runs[False], runs[True]):
+        for k in ("accepted", "rejected_err", "rejected_nl", "newton_iters", "setups"):
+            assert sc[k] == sf[k], k
+        assert abs(sf["t"] - sc["t"]) <= 1e-15
+        assert rel(yf, yc) <= 1e-9
+    assert runs[True][2][0]["accepted"] == runs[True][1][0]["accepted"]      # t_end already reached
+    assert np.array_equal(runs[True][2][1], runs[True][1][1])
+    # a whole-interval oracle run agrees on the final time (states differ:
+    # the intermediate t_end clip the step sequence)
+    assert abs(runs[True][3][0]["t"] - 0.004) <= 1e-15
