@@ -1,3 +1,9 @@
-SUNBW_DEBUG=1 timeout 300 python -m pytest tests/test_gpu_fused_tol.py -q -p no:cacheprovider -k multirank -x 2>&1 | grep -E "sunbw|passed|failed" | head
-SUNBW_PEER_HALO=0 timeout 300 python -m pytest tests/test_gpu_fused_tol.py -q -p no:cacheprovider -k multirank -x 2>&1 | tail -1
-SUNBW_DEBUG=1 timeout 300 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_fused_tol.py -q -p no:cacheprovider -k multirank -x 2>&1 | grep -v "^    " | head -40
+SUNBW_LIB=$PWD/build/var_pf2/libsunbw.so timeout 600 python -m pytest tests/test_gpu_contracted.py -q -p no:cacheprovider -x 2>&1 | tail -1
+for i in 1 2 3; do
+  for v in def pf1 pf2; do
+    if [ $v = def ]; then L=""; else L="SUNBW_LIB=$PWD/build/var_$v/libsunbw.so"; fi
+    env $L timeout 300 python bench.py --steps 200 --warmup 5 --no-ops --no-cpu > gpurun_out/ab_${v}_${i}.json 2>/dev/null
+    python -c "import json;d=json.load(open('gpurun_out/ab_${v}_${i}.json'));print('$v',d['kernels']['fused_newton']['us_avg'],round(d['value']/1e9,2))"
+  done
+done
+SUNBW_LIB=$PWD/build/var_pf2/libsunbw.so timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:fused_newton -s 3 -c 1 python bench.py --steps 5 --warmup 3 --no-ops --no-cpu 2>&1 | grep -E "dram__|gpu__time"
