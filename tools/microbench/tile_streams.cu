@@ -143,6 +143,73 @@ __global__ void __launch_bounds__(kCells, 5) k_tiles(const double* y, const doub
   if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// mode 6: the SBDF2 step without the history vector — y_n and y_{n-1} each
+// with their row-below and plane-below tiles in (the history term is
+// recomputed from y_{n-1} and its stencil), y_{n+1} out (3 streams + 4
+// neighbour tiles, 72 B/cell algorithmic); chain > 0 adds the dependent
+// DFMA chains of mode 2.  L2 hints as in mode 5.
+struct __align__(128) Smem6 {
+  double in[2][6][kTile];
+  double xm[2][2][8];
+  double out[2][kTile];
+  uint64_t full[2];
+};
+__global__ void __launch_bounds__(kCells, 5) k_tiles6(const double* y, const double* yp, double* z, int64_t ntiles,
+                                                       int64_t row_tiles, int64_t plane_tiles, int chain) {
+  extern __shared__ __align__(128) unsigned char raw[];
+  Smem6& S = *reinterpret_cast<Smem6*>(raw);
+  const int t = threadIdx.x;
+  const uint64_t PL = pol_last(), PF = pol_first();
+  auto issue = [&](int64_t tile, int st) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&S.full[st])),
+                 "r"(6 * kTile * 8 + 2 * 48) : "memory");
+    const int64_t ym = tile >= row_tiles ? tile - row_tiles : tile;
+    const int64_t zm = tile >= plane_tiles ? tile - plane_tiles : tile + ntiles - plane_tiles;
+    const int64_t xp = tile > 0 ? tile * kTile - 6 : 0;
+    g2s_h(S.in[st][0], y + tile * kTile, kTile * 8, &S.full[st], PL);
+    g2s_h(S.in[st][1], y + ym * kTile, kTile * 8, &S.full[st], PL);
+    g2s_h(S.in[st][2], y + zm * kTile, kTile * 8, &S.full[st], PF);
+    g2s(S.xm[st][0], y + xp, 48, &S.full[st]);
+    g2s_h(S.in[st][3], yp + tile * kTile, kTile * 8, &S.full[st], PL);
+    g2s_h(S.in[st][4], yp + ym * kTile, kTile * 8, &S.full[st], PL);
+    g2s_h(S.in[st][5], yp + zm * kTile, kTile * 8, &S.full[st], PF);
+    g2s(S.xm[st][1], yp + xp, 48, &S.full[st]);
+  };
+  if (t == 0) {
+    for (int s = 0; s < 2; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&S.full[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int s = 0; s < 2; ++s)
+      if (blockIdx.x + s * (int64_t)gridDim.x < ntiles) issue(blockIdx.x + s * (int64_t)gridDim.x, s);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it & 1;
+    asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(
+                     sa(&S.full[st])), "r"((uint32_t)((it >> 1) & 1)) : "memory");
+    const int ob = it & 1;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      double a = __dadd_rn(S.in[st][0][3 * t + s], __dadd_rn(S.in[st][1][3 * t + s], S.in[st][2][3 * t + s]));
+      double b = __dadd_rn(S.in[st][3][3 * t + s], __dadd_rn(S.in[st][4][3 * t + s], S.in[st][5][3 * t + s]));
+      a = __dadd_rn(a, t > 0 ? S.in[st][0][3 * (t - 1) + s] : S.xm[st][0][3 + s]);
+      b = __dadd_rn(b, t > 0 ? S.in[st][3][3 * (t - 1) + s] : S.xm[st][1][3 + s]);
+      for (int c = 0; c < chain; ++c) a = __fma_rn(a, 0.999999, b);
+      S.out[ob][3 * t + s] = __dadd_rn(a, b);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+      s2g_h(z + tile * kTile, S.out[ob], kTile * 8, PF);
+      const int64_t nx = tile + 2 * (int64_t)gridDim.x;
+      if (nx < ntiles) issue(nx, st);
+    }
+  }
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main(int argc, char** argv) {
   const int64_t n = 256, G = n * n * n, ntiles = G / kCells;
   double *y, *h, *z, *ho;
@@ -172,6 +239,26 @@ int main(int argc, char** argv) {
     const double us = ms * 1e3 / reps;
     printf("mode %d chain %3d (3 chains/thread): %7.1f us/launch  %6.0f GB/s algorithmic (96 B/cell)  err=%s\n",
            c.mode, c.chain, us, 96.0 * G / (us * 1e-6) / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    const int smem6 = sizeof(Smem6);
+    cudaFuncSetAttribute(k_tiles6, cudaFuncAttributeMaxDynamicSharedMemorySize, smem6);
+    for (int chain : {0, 32}) {
+      if (only >= 0 && only != 6) break;
+      for (int w = 0; w < 3; ++w) k_tiles6<<<grid, kCells, smem6>>>(y, h, z, ntiles, 2, 512, chain);
+      cudaEventRecord(e0);
+      const int reps = 20;
+      // rotation y_{n-1} <- y_n <- y_{n+1} over three buffers
+      double* buf[3] = {h, y, z};
+      for (int r = 0; r < reps; ++r)
+        k_tiles6<<<grid, kCells, smem6>>>(buf[(r + 1) % 3], buf[r % 3], buf[(r + 2) % 3], ntiles, 2, 512, chain);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      const double us = ms * 1e3 / reps;
+      printf("mode 6 chain %3d (no history vector): %7.1f us/launch  %6.0f GB/s algorithmic (72 B/cell)  "
+             "err=%s\n", chain, us, 72.0 * G / (us * 1e-6) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   return 0;
 }
