@@ -216,6 +216,9 @@ class PinnedCore:
                 "cpu_model": cpu_model(), "threads": "1 (serial oracle, pinned)"}
 
 
+REF_REPEATS = 3
+
+
 def oracle_c5_sample(steps, warmup=0, planes=REF_PLANES):
     """The oracle on the bench workload's sample: a 256 x 256 x planes
     periodic slab with the C5 parameters, SBDF + K = 3; returns (cell-steps/s,
@@ -228,9 +231,14 @@ def oracle_c5_sample(steps, warmup=0, planes=REF_PLANES):
     kw = dict(kind=0, K=3, nx=nx, ny=ny, nz=planes, kx=k, ky=k, kz=k, h=1e-3)
     if warmup:
         oracle.sbdf_integrate(y0, warmup, **kw)
-    t0 = time.perf_counter()
-    rc, _, _, _ = oracle.sbdf_integrate(y0, steps, **kw)
-    dt = time.perf_counter() - t0
+    # best of REF_REPEATS timed runs: a shared host's other tenants only ever
+    # slow a run down, so the fastest is the reproducible figure (both arms)
+    dts = []
+    for _ in range(REF_REPEATS):
+        t0 = time.perf_counter()
+        rc, _, _, _ = oracle.sbdf_integrate(y0, steps, **kw)
+        dts.append(time.perf_counter() - t0)
+    dt = min(dts)
     return nx * ny * planes * steps / dt, dt, rc
 
 
@@ -244,7 +252,7 @@ def run_reference(args, world, rank):
         v, dt, rc = oracle_c5_sample(args.steps, args.warmup, planes=args.ref_planes)
         desc = pc.describe()
     sample = (f"256x256x{args.ref_planes} cells (1/{256 // args.ref_planes} of a 256^3 slab), "
-              f"{args.steps} SBDF2 steps, K=3")
+              f"{args.steps} SBDF2 steps, K=3, best of {REF_REPEATS} timed runs")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "cell-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
