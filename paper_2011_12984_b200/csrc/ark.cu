@@ -21,6 +21,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <utility>
 #include <vector>
 
 #include "sunbw_internal.h"
@@ -174,6 +175,43 @@ int attempt(Ark* A, int* nl_ok, double* dsm) {
   return e;
 }
 
+// BW_ArkEvolve's loop with host decisions (composed path): *rc = 0, 1
+// (max_steps) or 2 (step size underflow); < 0 on errors.
+int evolve_host(Ark* A, double t_end, int* rc) {
+  int attempts = 0;
+  while (t_end - A->t > 1e-12 * std::fmax(1.0, std::fabs(t_end))) {
+    if (attempts++ >= A->opt.max_steps) { *rc = 1; break; }
+    // a step shortened to land on t_end does not shrink the next proposal
+    // (DESIGN R26): the unclipped h is restored after it if larger
+    const double h_unclipped = A->h;
+    const bool clipped = A->t + A->h > t_end;
+    if (clipped) A->h = t_end - A->t;
+    if (A->h < 1e-14 * (1.0 + A->t)) { *rc = 2; break; }
+    int nl_ok = 1;
+    double dsm = 0.0;
+    int e = attempt(A, &nl_ok, &dsm);
+    if (e < 0) return e;
+    if (!nl_ok) {
+      A->st.rejected_nl++;
+      A->h *= 0.25;
+      continue;
+    }
+    double fac = dsm > 0.0 ? 0.9 * std::pow(dsm, -1.0 / 3.0) : 5.0;
+    if (A->opt.fixed) { dsm = 0.0; fac = 1.0; }
+    if (dsm <= 1.0) {
+      std::swap(A->y, A->ynew);
+      A->t += A->h;
+      A->st.accepted++;
+      A->h *= std::fmin(5.0, std::fmax(0.2, fac));
+      if (clipped) A->h = std::fmax(A->h, h_unclipped);
+    } else {
+      A->st.rejected_err++;
+      A->h *= std::fmin(1.0, std::fmax(0.2, fac));
+    }
+  }
+  return 0;
+}
+
 }  // namespace
 
 extern "C" int BW_ArkCreate(void* prob, N_Vector y0, const BW_ArkOptions* opt, void** out) {
@@ -219,42 +257,10 @@ extern "C" int BW_ArkEvolve(void* ark, double t_end, N_Vector y_out, BW_ArkStats
   SUNBW_Context ctx = A->ctx;
   if (y_out && (y_out->ctx != ctx || y_out->local_len != A->n)) return ctx_set_err(ctx, SUNBW_ERR_LENGTH);
   int rc = 0;
-  int attempts = 0;
-  if (A->fused) {                                // the same loop, decided on the device (R33)
-    if (int e = sunbw::ark_fused_evolve(A->fused, &A->y, &A->ynew, &A->t, &A->h, t_end, A->opt, &A->st, &rc))
-      return e;
-    attempts = -1;                               // (loop below skipped)
-  }
-  while (attempts >= 0 && t_end - A->t > 1e-12 * std::fmax(1.0, std::fabs(t_end))) {
-    if (attempts++ >= A->opt.max_steps) { rc = 1; break; }
-    // a step shortened to land on t_end does not shrink the next proposal
-    // (DESIGN R26): the unclipped h is restored after it if larger
-    const double h_unclipped = A->h;
-    const bool clipped = A->t + A->h > t_end;
-    if (clipped) A->h = t_end - A->t;
-    if (A->h < 1e-14 * (1.0 + A->t)) { rc = 2; break; }
-    int nl_ok = 1;
-    double dsm = 0.0;
-    int e = attempt(A, &nl_ok, &dsm);
-    if (e < 0) return e;
-    if (!nl_ok) {
-      A->st.rejected_nl++;
-      A->h *= 0.25;
-      continue;
-    }
-    double fac = dsm > 0.0 ? 0.9 * std::pow(dsm, -1.0 / 3.0) : 5.0;
-    if (A->opt.fixed) { dsm = 0.0; fac = 1.0; }
-    if (dsm <= 1.0) {
-      std::swap(A->y, A->ynew);
-      A->t += A->h;
-      A->st.accepted++;
-      A->h *= std::fmin(5.0, std::fmax(0.2, fac));
-      if (clipped) A->h = std::fmax(A->h, h_unclipped);
-    } else {
-      A->st.rejected_err++;
-      A->h *= std::fmin(1.0, std::fmax(0.2, fac));
-    }
-  }
+  const int e = A->fused ? sunbw::ark_fused_evolve(A->fused, &A->y, &A->ynew, &A->t, &A->h, t_end, A->opt,
+                                                   &A->st, &rc)   // the same loop, decided on the device (R33)
+                         : evolve_host(A, t_end, &rc);
+  if (e < 0) return e;
   if (y_out &&
       cudaMemcpyAsync(y_out->d, A->y, sizeof(double) * A->n, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
