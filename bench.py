@@ -638,6 +638,13 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
+    # the oracle baseline first, while this process has not touched the GPU:
+    # measured after the GPU work (with this process's CUDA context, 2.4 GB
+    # of pinned buffers and the device at full power) the same subprocess
+    # ran 1.6x slower than the standalone reference arm (r02s/r02t)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_sample(min(args.steps, 60), max(args.warmup, 3))
 
     import torch
     import torch.distributed as dist
@@ -812,9 +819,6 @@ def main():
     if rank == 0 and world == 1 and not args.no_ops:
         torch.cuda.empty_cache()
         configs = other_configs(S, ctx, torch)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample(min(args.steps, 60), max(args.warmup, 3))
 
     if rank == 0:
         line = {
