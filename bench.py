@@ -487,7 +487,8 @@ def other_configs(S, ctx, torch):
         "fused_steps_per_s": round(rt, 1), "cell_steps_per_s": rt * 256 ** 3,
         "newton_iters_per_step": round(stt["newton_iters"] / stt["steps"], 3),
         "launches_per_step": round(stt["setups"] / stt["steps"], 3),
-        "note": "newton_mode=1, tol_nl=1e-3, K<=5, contracted cell step; one host decision per step (R31)"}
+        "note": "newton_mode=1, tol_nl=1e-3, K<=5, contracted cell step; the oracle's per-step decision "
+                "(R31) taken by the step kernel's last CTA, no host synchronisation inside Advance (R35)"}
     c3 = S.bruss_params(dim=3, nx=128, ny=128, nz=128)
     r3 = stepper_rate(c3, 128 ** 3, 200, use_graph=True, fused=True)
     out["C3_3D_128cubed"] = {"fused_steps_per_s": round(r3, 1), "cell_steps_per_s": r3 * 128 ** 3}

@@ -46,7 +46,7 @@ int fused_newton(SUNBW_Context ctx, void* prob, int64_t G, bool first, int K, do
                  double rtol, double atol, const double* y, const double* fE, const double* hin,
                  double* hout, double* z, double* partials, unsigned long long* d_first,
                  int* nblocks_out, const FusedAdvection* adv, int64_t tile_begin, int64_t tile_end,
-                 const FusedFold* fold, int solver, bool tol);
+                 const FusedFold* fold, int solver, bool tol, TolDev* tdev = nullptr);
 int fused_fold(SUNBW_Context ctx, const double* partials, int nblocks, int K, int64_t nglobal,
                double* d_min, double* d_nu, int* d_err);
 int fused_finalize_pending(SUNBW_Context ctx, double* pending, int K, int64_t nglobal, double* d_min,
@@ -101,6 +101,11 @@ struct Stepper {
   double* h_tol = nullptr;   // fused tolerance mode: pinned [min, nu_1..nu_8 | first | err]
   unsigned long long* h_end = nullptr;   // pinned: end-of-Advance [first, err, nu]
   int k_pred = 0;            // fused tolerance mode: the last step's iteration count
+  sunbw::TolDev* d_tdev = nullptr;   // fused tolerance mode driven from the device (R35)
+  sunbw::TolDev* h_tdev = nullptr;   // pinned staging
+  int* h_tdone = nullptr;            // mapped pinned: TolDev::done after the latest launch
+  int* d_tdone = nullptr;
+  cudaEvent_t tev[2] = {};
   int64_t tol_launches = 0;  // fused tolerance mode: step launches (recomputations included)
   unsigned* d_counter = nullptr;   // fused mode: arrival counter of the in-kernel fold
   SUNLinearSolver gm = nullptr;   // linsol 1: SPGMR, block-LU preconditioner
@@ -635,6 +640,17 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
   if (!e && opt->fused && opt->newton_mode == 1 &&
       cudaHostAlloc(&S->h_tol, sizeof(double) * (kMaxKF + 4), cudaHostAllocDefault) != cudaSuccess)
     e = SUNBW_ERR_MEM;
+  sunbw::FusedAdvection fa_t;
+  const bool adv_fused = opt->fused && opt->fused_advection && sunbw::bw_fused_advection(prob, y0->d, &fa_t) &&
+                         G % 128 == 0 && G <= INT32_MAX;
+  if (!e && opt->fused && opt->newton_mode == 1 && ctx_nranks(ctx) == 1 && adv_fused &&
+      (cudaMalloc(&S->d_tdev, sizeof(sunbw::TolDev)) != cudaSuccess ||
+       cudaHostAlloc(&S->h_tdev, sizeof(sunbw::TolDev), cudaHostAllocDefault) != cudaSuccess ||
+       cudaHostAlloc(&S->h_tdone, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+       cudaHostGetDevicePointer((void**)&S->d_tdone, S->h_tdone, 0) != cudaSuccess ||
+       cudaEventCreateWithFlags(&S->tev[0], cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&S->tev[1], cudaEventDisableTiming) != cudaSuccess))
+    e = SUNBW_ERR_MEM;
   if (e) {
     cudaGetLastError();
     BW_StepperDestroy(S);
@@ -648,6 +664,74 @@ extern "C" int BW_StepperCreate(void* prob, N_Vector y0, const BW_StepperOptions
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
   }
   *out = S;
+  return 0;
+}
+
+// Fused tolerance mode, one rank, in-kernel advection, after the first
+// step (R35): up to n steps with the decisions on the device.  Each launch is
+// one attempt of the current step (the kernel takes its buffers and
+// iteration count from TolDev, its last CTA decides); the host keeps two
+// launches in flight and stops enqueuing once the mapped done flag is set
+// (at most one no-op launch follows).  *done = steps completed; *rc = the
+// recoverable code of a failed step (the Advance ends there), else 0.
+int tol_device_advance(Stepper* S, int64_t n, int64_t* done, int* rc) {
+  SUNBW_Context ctx = S->ctx;
+  const BW_StepperOptions& o = S->opt;
+  sunbw::FusedAdvection fa;
+  if (!sunbw::bw_fused_advection(S->prob, S->y[S->iy], &fa)) return ctx_set_err(ctx, SUNBW_ERR_ARG);
+  sunbw::TolDev& T = *S->h_tdev;
+  std::memset(&T, 0, sizeof(T));
+  for (int i = 0; i < 3; ++i) T.y[i] = S->y[i];
+  for (int i = 0; i < 2; ++i) T.H[i] = S->fE[i];
+  T.iy = S->iy; T.iyp = S->iyp; T.iz = S->iz; T.ife = S->ife; T.ifep = S->ifep;
+  T.K = o.K;
+  T.Kr = S->k_pred > 0 && S->k_pred <= o.K ? S->k_pred : o.K;
+  T.k_pred = S->k_pred;
+  T.nsteps = n;
+  T.tol_nl = o.tol_nl;
+  T.below_off = (long long)(fa.below - S->y[S->iy]);
+  T.host_done = S->d_tdone;
+  *(volatile int*)S->h_tdone = 0;
+  if (cudaMemcpyAsync(S->d_tdev, &T, sizeof(T), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  const int64_t max_launches = 3 * n + 2;            // <= 3 attempts per step
+  for (int64_t k = 0;; ++k) {
+    if (k > max_launches) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    int nb = 0;
+    sunbw::FusedFold fold{0, S->d_counter, nullptr, S->d_scal, S->d_scal + 1, S->d_err, S->nglobal};
+    {
+      Timed t(S, BW_K_FUSED_NEWTON);
+      // (pointer arguments: placeholders of the right shape; the kernel takes
+      // the current ones from TolDev)
+      TRY(sunbw::fused_newton(ctx, S->prob, S->G, false, o.K, o.h, o.rtol, o.atol, S->y[S->iy], nullptr,
+                              S->fE[S->ifep], S->fE[S->ife], S->y[S->iz], S->d_partials, S->d_first, &nb, &fa, 0,
+                              -1, &fold, 2, true, S->d_tdev));
+    }
+    if (cudaEventRecord(S->tev[k & 1], ctx->stream) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+    if (k > 0) {
+      if (cudaEventSynchronize(S->tev[(k - 1) & 1]) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+      if (*(volatile int*)S->h_tdone) break;
+    }
+  }
+  if (cudaMemcpyAsync(&T, S->d_tdev, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    return ctx_set_err(ctx, SUNBW_ERR_CUDA);
+  if (T.rc < 0) return ctx_set_err(ctx, T.rc);
+  S->iy = T.iy; S->iyp = T.iyp; S->iz = T.iz; S->ife = T.ife; S->ifep = T.ifep;
+  S->k_pred = T.k_pred;
+  S->tol_launches += T.attempts;
+  S->step += T.steps_done;
+  S->t += (double)T.steps_done * o.h;
+  S->st.steps += T.steps_done;
+  S->st.setups += T.steps_done + T.setups_extra;
+  S->st.newton_iters += T.newton_iters;
+  if (T.steps_done > 0 || T.rc == SUNBW_RECOV_NONCONV) S->st.last_nu = T.last_nu;
+  if (T.rc > 0) {
+    S->st.fails++;
+    if (T.rc == SUNBW_RECOV_SINGULAR) S->st.singular = (int64_t)T.singular;
+  }
+  *done = T.steps_done;
+  *rc = T.rc;
   return 0;
 }
 
@@ -680,6 +764,12 @@ extern "C" int BW_StepperAdvance(void* stepper, int64_t nsteps, N_Vector y_out, 
   const int64_t nloop = S->small ? 0 : nsteps;  // per-step launches
   for (int64_t s = 0; s < nloop;) {
     bool first = S->step == 0;
+    if (!first && S->d_tdev) {                      // the rest of the Advance on the device (R35)
+      int64_t nd = 0;
+      TRY(tol_device_advance(S, nloop - s, &nd, &rc));
+      s += nd;
+      break;
+    }
     int nin = 1;                                  // steps done by this iteration
     if (S->opt.use_graph && !first) {
       int key = graph_key(S);
@@ -827,6 +917,11 @@ extern "C" int BW_StepperDestroy(void* stepper) {
   if (S->evB) cudaEventDestroy(S->evB);
   if (S->d_pending) cudaFree(S->d_pending);
   if (S->h_tol) cudaFreeHost(S->h_tol);
+  if (S->d_tdev) cudaFree(S->d_tdev);
+  if (S->h_tdev) cudaFreeHost(S->h_tdev);
+  if (S->h_tdone) cudaFreeHost(S->h_tdone);
+  for (auto ev : S->tev)
+    if (ev) cudaEventDestroy(ev);
   if (S->h_end) cudaFreeHost(S->h_end);
   delete S;
   return 0;

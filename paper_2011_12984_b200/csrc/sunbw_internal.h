@@ -227,6 +227,25 @@ void ark_fused_destroy(ArkFused* F);
 int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* h, double t_end,
                      const BW_ArkOptions& opt, BW_ArkStats* st, int* rc);
 
+// Fused tolerance mode driven from the device (DESIGN R35; one rank, in-
+// kernel advection): the rotation of the state buffers, the iteration count
+// of the next launch and the step's decision live here; the step kernel
+// reads them at entry and its last CTA takes the oracle's decision (R31)
+// after folding the norms, so the host enqueues launches without waiting.
+struct TolDev {
+  double* y[3];              // state buffers (S->y)
+  double* H[2];              // SBDF2 history buffers (S->fE)
+  int iy, iyp, iz, ife, ifep;
+  int Kr, K, k_pred;
+  int done, rc;              // rc: 0 or SUNBW_RECOV_*
+  int attempt;               // launches of the current step so far
+  long long nsteps, steps_done, newton_iters, setups_extra, attempts;
+  unsigned long long singular;
+  double last_nu, tol_nl;
+  long long below_off;       // y + below_off: the plane under local plane 0 (own wrap)
+  volatile int* host_done;   // mapped pinned: done after the latest launch
+};
+
 struct FusedFold {
   int prev_parts;            // partial rows written by earlier launches of this step
   unsigned* counter;         // zero-initialised

@@ -73,6 +73,24 @@ def test_fused_tol_3D_in_kernel_advection(S, ctx):
     assert rel_err(ys[-1], yref) <= 1e-9
 
 
+@pytest.mark.parametrize("chunk", [1, 7, 30])
+def test_fused_tol_device_driven_chunks(S, ctx, chunk):
+    """One rank with the in-kernel advection: after the first step the
+    decisions run on the device (DESIGN R35).  Advance calls of 1, 7 and 30
+    steps (the rotation state, the iteration prediction and the statistics
+    carry across calls) give the oracle's iteration count and state."""
+    nx, ny, nz, steps = 128, 6, 4, 30
+    y0 = oracle.bruss_ic(nx, ny, nz)
+    k = kappas(nx, ny, nz)
+    rc, ys, st = run_fused_tol(S, ctx, S.bruss_params(dim=3, nx=nx, ny=ny, nz=nz), y0, steps, chunk,
+                               h=1e-3, K=5, tol_nl=1e-5)
+    _, yref, stref, _ = oracle.sbdf_integrate(y0, steps, kind=0, newton_mode=1, K=5, nx=nx, ny=ny, nz=nz,
+                                              kx=k[0], ky=k[1], kz=k[2], h=1e-3, tol_nl=1e-5)
+    assert rc == 0 and st["steps"] == steps
+    assert st["newton_iters"] == stref["newton_iters"], (st["newton_iters"], stref["newton_iters"])
+    assert rel_err(ys[-1], yref) <= 1e-9
+
+
 def test_fused_tol_C3(S, ctx):
     """C3 (128^3 cells), 10 steps: the bench-shaped 3D grid."""
     n, steps = 128, 10
