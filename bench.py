@@ -561,7 +561,7 @@ def other_configs(S, ctx, torch):
     return out
 
 
-E2E_ADVANCES = 16
+E2E_ADVANCES = 24
 
 
 def e2e_pipelined(torch, S, ctx, st, host_y0, K, n_adv):
