@@ -562,16 +562,20 @@ def other_configs(S, ctx, torch):
 
 
 E2E_ADVANCES = 24
+E2E_SPLIT = 1
 
 
-def e2e_pipelined(torch, S, ctx, st, host_y0, K, n_adv):
+def e2e_pipelined(torch, S, ctx, st, host_y0, K, n_adv, split=None):
     """Ensemble e2e: n_adv independent problems (y0 perturbed per problem)
-    through Stepper.reset / Stepper.advance with host buffers.  H2D on one
-    copy stream, D2H on another, the stepper on the context stream; two
-    device buffers each way.  Returns (device ms from the first H2D to the
-    last D2H, n_adv)."""
+    through Stepper.reset / Stepper.advance with host buffers.  H2D on
+    `split` copy streams (one contiguous part each), D2H likewise, the
+    stepper on the context stream; two device buffers each way.  Returns
+    (device ms from the first H2D to the last D2H, n_adv)."""
+    if split is None:
+        split = int(os.environ.get("SUNBW_E2E_SPLIT", str(E2E_SPLIT)))
     comp = ctx.stream
-    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    h2d = [torch.cuda.Stream() for _ in range(split)]
+    d2h = [torch.cuda.Stream() for _ in range(split)]
     hin = [host_y0.clone().pin_memory() for _ in range(2)]
     hin[1].mul_(1.0 + 1e-3)
     hout = [torch.empty_like(host_y0).pin_memory() for _ in range(2)]
@@ -579,38 +583,51 @@ def e2e_pipelined(torch, S, ctx, st, host_y0, K, n_adv):
     dout = [torch.empty_like(d) for d in din]
     vin = [S.NVector(ctx, d) for d in din]
     vout = [S.NVector(ctx, d) for d in dout]
+    n = host_y0.numel()
+    cuts = [n * i // split for i in range(split + 1)]
+    parts = lambda t: [t[cuts[i]:cuts[i + 1]] for i in range(split)]  # noqa: E731
     ev = lambda: torch.cuda.Event()  # noqa: E731
-    in_ready, in_free, out_ready, out_free = ([ev(), ev()] for _ in range(4))
+    in_ready = [[ev() for _ in range(split)] for _ in range(2)]
+    out_free = [[ev() for _ in range(split)] for _ in range(2)]
+    in_free, out_ready = [ev(), ev()], [ev(), ev()]
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(comp)
-    h2d.wait_event(t0)
+    for q in h2d:
+        q.wait_event(t0)
 
     def load(r):
         b = r % 2
-        with torch.cuda.stream(h2d):
-            if r >= 2:
-                h2d.wait_event(in_free[b])          # the stepper has copied problem r-2 in
-            din[b].copy_(hin[b], non_blocking=True)
-            in_ready[b].record(h2d)
+        for i, (q, dst, src) in enumerate(zip(h2d, parts(din[b]), parts(hin[b]))):
+            with torch.cuda.stream(q):
+                if r >= 2:
+                    q.wait_event(in_free[b])         # the stepper has copied problem r-2 in
+                dst.copy_(src, non_blocking=True)
+                in_ready[b][i].record(q)
 
     load(0)
     for r in range(n_adv):
         b = r % 2
         if r + 1 < n_adv:
             load(r + 1)                              # prefetch under this Advance
-        comp.wait_event(in_ready[b])
+        for e in in_ready[b]:
+            comp.wait_event(e)
         if r >= 2:
-            comp.wait_event(out_free[b])             # problem r-2's result has left
+            for e in out_free[b]:
+                comp.wait_event(e)                   # problem r-2's result has left
         st.reset(vin[b], 0.0)
         in_free[b].record(comp)
         rc, _ = st.advance(K, vout[b])
         assert rc == 0, rc
         out_ready[b].record(comp)
-        with torch.cuda.stream(d2h):
-            d2h.wait_event(out_ready[b])
-            hout[b].copy_(dout[b], non_blocking=True)
-            out_free[b].record(d2h)
+        for i, (q, dst, src) in enumerate(zip(d2h, parts(hout[b]), parts(dout[b]))):
+            with torch.cuda.stream(q):
+                q.wait_event(out_ready[b])
+                dst.copy_(src, non_blocking=True)
+                out_free[b][i].record(q)
+    for q in d2h[1:]:
+        d2h[0].wait_stream(q)
+    d2h = d2h[0]
     t1.record(d2h)
     torch.cuda.synchronize()
     assert torch.isfinite(hout[0]).all() and torch.isfinite(hout[1]).all()
