@@ -166,3 +166,21 @@ def test_ark_fused_successive_evolve_calls(S, ctx, shape):
     # a whole-interval oracle run agrees on the final time (states differ:
     # the intermediate t_end clip the step sequence)
     assert abs(runs[True][3][0]["t"] - 0.004) <= 1e-15
+
+
+def test_ark_fused_C3_bench_configuration(S, ctx):
+    """The bench's ARK row at full size and in its launch configuration:
+    C3 (128^3 cells, TMA-tiled stage kernels, device-driven rounds with the
+    P = 1 round graph) to t = 0.01 from h0 = 1e-4 — the same accepted /
+    rejected / Newton / setup counts as the oracle and the state within
+    1e-9 (the oracle takes ~40-60 s here)."""
+    n = 128
+    y0 = oracle.bruss_ic(n, n, n)
+    rc2, yref, st2 = oracle.ark_integrate(y0, 0.01, h0=1e-4, max_steps=2000, nx=n, ny=n, nz=n, kx=0.01 * n,
+                                          ky=0.01 * n, kz=0.01 * n)
+    rc, y, st = run(S, ctx, S.bruss_params(dim=3, nx=n, ny=n, nz=n), y0, 0.01, h0=1e-4, max_steps=2000,
+                    fused=True)
+    assert rc == rc2 == 0
+    for key in ("accepted", "rejected_err", "rejected_nl", "newton_iters", "setups"):
+        assert st[key] == st2[key], key
+    assert rel(y, yref) <= 1e-9
