@@ -136,7 +136,11 @@ struct Stepper {
   // timing
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<int> ev_kind;
+  std::vector<int> ev_kind;          // per event pair: kind + kKindMod * (launches - 1)
+  // fused single-kernel steps captured as a chain: one event pair around the
+  // whole chain instead of one per kernel (an event-record node between two
+  // step kernels costs ~7 us of idle GPU, tools/step_gaps_cupti.py)
+  bool chain_timed = false;
   double k_ms[BW_K_COUNT_] = {};
   int64_t k_count[BW_K_COUNT_] = {};
 };
@@ -164,13 +168,17 @@ const char* nvtx_category(int kind) {
   }
 }
 
+constexpr int kKindMod = 64;              // > BW_K_COUNT_
+static_assert(BW_K_COUNT_ < kKindMod, "event kind encoding");
+
 struct Timed {
   Stepper* S;
   int kind;
   bool on;
   cudaStream_t st;
   Timed(Stepper* s, int k, cudaStream_t stream = nullptr)
-      : S(s), kind(k), on(s->opt.timing != 0), st(stream ? stream : s->ctx->stream) {
+      : S(s), kind(k), on(s->opt.timing != 0 && !(s->chain_timed && k == BW_K_FUSED_NEWTON)),
+        st(stream ? stream : s->ctx->stream) {
     nvtxRangePushA(nvtx_category(k));
     if (!on) return;
     if (S->ev_used + 2 > S->ev_pool.size()) {
@@ -197,8 +205,9 @@ void harvest_timing(Stepper* S) {
   for (size_t i = 0; i < S->ev_kind.size(); ++i) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, S->ev_pool[2 * i], S->ev_pool[2 * i + 1]);
-    S->k_ms[S->ev_kind[i]] += ms;
-    S->k_count[S->ev_kind[i]]++;
+    const int kind = S->ev_kind[i] % kKindMod, launches = S->ev_kind[i] / kKindMod + 1;
+    S->k_ms[kind] += ms;
+    S->k_count[kind] += launches;
   }
   S->ev_kind.clear();
   S->ev_used = 0;
@@ -497,9 +506,37 @@ int capture_step(Stepper* S, int key, int nsteps = 1) {
   } else {
     S->capturing = true;
     const int iy = S->iy, iyp = S->iyp, iz = S->iz, ife = S->ife, ifep = S->ifep;
+    // one kernel per step (fused with the in-kernel advection, one rank,
+    // fixed K): time the chain as a whole; the kernels follow each other
+    // with ~0.3 us gaps, so the pair's time / nsteps is the kernel's launch
+    // duration to within that.  The pair is reserved (and its kind entered)
+    // before the steps are enqueued, so it keeps its place in the pool.
+    sunbw::FusedAdvection fa;
+    bool chain = S->opt.timing && S->opt.fused && S->opt.newton_mode == 0 && S->opt.fused_advection &&
+                 ctx_nranks(ctx) <= 1 && nsteps > 1 && S->G % 128 == 0 && S->G <= INT32_MAX &&
+                 sunbw::bw_fused_advection(S->prob, S->y[S->iy], &fa);
+    size_t slot = 0;
+    if (chain) {
+      while (S->ev_used + 2 > S->ev_pool.size() && chain) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) { rc = SUNBW_ERR_CUDA; chain = false; break; }
+        S->ev_pool.push_back(e);
+      }
+    }
+    if (chain) {
+      slot = S->ev_used;
+      S->ev_used += 2;
+      S->ev_kind.push_back(BW_K_FUSED_NEWTON + kKindMod * (nsteps - 1));
+      cudaEventRecordWithFlags(S->ev_pool[slot], S->cap_stream, cudaEventRecordExternal);
+      S->chain_timed = true;
+    }
     for (int k = 0; k < nsteps && !rc; ++k) {
       rc = enqueue_step(S, false);
       rotate(S);
+    }
+    if (chain) {
+      S->chain_timed = false;
+      cudaEventRecordWithFlags(S->ev_pool[slot + 1], S->cap_stream, cudaEventRecordExternal);
     }
     S->iy = iy; S->iyp = iyp; S->iz = iz; S->ife = ife; S->ifep = ifep;
     S->capturing = false;
