@@ -561,7 +561,7 @@ def other_configs(S, ctx, torch):
     return out
 
 
-E2E_ADVANCES = 24
+E2E_ADVANCES = 48
 E2E_SPLIT = 1
 
 
