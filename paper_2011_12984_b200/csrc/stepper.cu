@@ -177,7 +177,9 @@ struct Timed {
   bool on;
   cudaStream_t st;
   Timed(Stepper* s, int k, cudaStream_t stream = nullptr)
-      : S(s), kind(k), on(s->opt.timing != 0 && !(s->chain_timed && k == BW_K_FUSED_NEWTON)),
+      : S(s), kind(k),
+        on(s->opt.timing != 0 && !(s->chain_timed && k == BW_K_FUSED_NEWTON) &&
+           (s->opt.timing <= 1 || s->capturing || s->step % s->opt.timing == 0)),
         st(stream ? stream : s->ctx->stream) {
     nvtxRangePushA(nvtx_category(k));
     if (!on) return;
