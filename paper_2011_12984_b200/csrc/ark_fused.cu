@@ -712,7 +712,7 @@ struct ArkFused {
   unsigned long long* first = nullptr;
   ArkCtl* ctl = nullptr;         // device controller state
   ArkCtl* h_ctl = nullptr;       // pinned staging for the controller state
-  int* h_done = nullptr;         // mapped pinned: ArkCtl::done after the latest round
+  int* h_done = nullptr;         // mapped pinned [2]: ArkCtl::done after round k in slot k & 1
   int* d_done = nullptr;         // ... its device address
   cudaEvent_t ev[2] = {};
   cudaStream_t cap = nullptr;    // P = 1: one round captured as a graph (per y buffer pair)
@@ -751,7 +751,7 @@ ArkFused* ark_fused_create(SUNBW_Context ctx, void* prob, int64_t nglobal) {
        cudaMalloc(&F->first, sizeof(unsigned long long) * kStages) == cudaSuccess &&
        cudaMalloc(&F->ctl, sizeof(ArkCtl)) == cudaSuccess &&
        cudaHostAlloc(&F->h_ctl, sizeof(ArkCtl), cudaHostAllocDefault) == cudaSuccess &&
-       cudaHostAlloc(&F->h_done, sizeof(int), cudaHostAllocMapped) == cudaSuccess &&
+       cudaHostAlloc(&F->h_done, 2 * sizeof(int), cudaHostAllocMapped) == cudaSuccess &&
        cudaHostGetDevicePointer((void**)&F->d_done, F->h_done, 0) == cudaSuccess &&
        cudaEventCreateWithFlags(&F->ev[0], cudaEventDisableTiming) == cudaSuccess &&
        cudaEventCreateWithFlags(&F->ev[1], cudaEventDisableTiming) == cudaSuccess &&
@@ -895,7 +895,7 @@ int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* 
   for (int i = 0; i < 3; ++i) c.kpred[i] = F->kpred[i];
   if (cudaMemcpyAsync(F->ctl, &c, sizeof(ArkCtl), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-  *(volatile int*)F->h_done = 0;
+  ((volatile int*)F->h_done)[0] = ((volatile int*)F->h_done)[1] = 0;
   k_ark_begin<<<1, 1, 0, s>>>(F->ctl, F->d_done);
   ctx->launches++;
   Args base{};
@@ -921,7 +921,10 @@ int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* 
     if (!multi || G0.expl != 0) return 0;
     return ctx->comm->halo_shift(wrap(v), dst, (size_t)G0.halo_len, s);
   };
-  auto round = [&]() -> int {
+  // slot: where this round's separate controller launch publishes done
+  // (P > 1: each rank must stop after the same round, so the host reads the
+  // state after round k - 1 — slot (k - 1) & 1 — not whatever is latest)
+  auto round = [&](int slot) -> int {
     for (int b = 0; b < 2; ++b)
       if (int e = exchange(yb[b], F->halo0[b])) return e;
     for (int i = 1; i <= 4; ++i) {
@@ -944,11 +947,11 @@ int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* 
       k_ark_pack<<<1, 32, 0, s>>>(F->ctl, F->first, F->sums);
       if (int e = ctx->comm->allreduce(F->sums, kStages * kCols, RED_SUM, s)) return e;
       k_ark_finalize<<<1, 32, 0, s>>>(F->ctl, F->sums, (double)F->nglobal, F->res);
-      k_ark_control<<<1, 1, 0, s>>>(F->ctl, F->res, F->d_done);
+      k_ark_control<<<1, 1, 0, s>>>(F->ctl, F->res, F->d_done + slot);
       ctx->launches += 3;
     } else if (G0.G == 0) {                      // (no final launch to carry the controller)
       k_ark_pack_finalize<<<1, 32, 0, s>>>(F->ctl, F->first, (double)F->nglobal, F->res, F->sums);
-      k_ark_control<<<1, 1, 0, s>>>(F->ctl, F->res, F->d_done);
+      k_ark_control<<<1, 1, 0, s>>>(F->ctl, F->res, F->d_done + slot);
       ctx->launches += 2;
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SUNBW_ERR_CUDA;
@@ -969,7 +972,7 @@ int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* 
     if (cudaStreamBeginCapture(F->cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       rc0 = SUNBW_ERR_CUDA;
     } else {
-      rc0 = round();
+      rc0 = round(0);                            // (one rank: the final launch publishes in slot 0)
       if (cudaStreamEndCapture(F->cap, &gr) != cudaSuccess && !rc0) rc0 = SUNBW_ERR_CUDA;
     }
     ctx->stream = s = user;
@@ -992,13 +995,13 @@ int ark_fused_evolve(ArkFused* F, double** y, double** ynew, double* t, double* 
     if (use_graph) {
       if (cudaGraphLaunch(F->gexec, s) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
       ctx->launches += F->glaunches;
-    } else if (int e = round()) {
+    } else if (int e = round((int)(k & 1))) {
       return ctx_set_err(ctx, e);
     }
     if (cudaEventRecord(F->ev[k & 1], s) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
     if (k > 0) {
       if (cudaEventSynchronize(F->ev[(k - 1) & 1]) != cudaSuccess) return ctx_set_err(ctx, SUNBW_ERR_CUDA);
-      if (*(volatile int*)F->h_done) break;
+      if (((volatile int*)F->h_done)[use_graph ? 0 : (int)((k - 1) & 1)]) break;
     }
   }
   if (cudaMemcpyAsync(&c, F->ctl, sizeof(ArkCtl), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
